@@ -1,0 +1,64 @@
+"""Build the in-tree CUDA library ``_lib/libqrmc_gpu.so`` for sm_100a.
+
+    python -m paper_2407_21084_b200.build
+
+nvcc cross-compiles here without a GPU; the .so is git-ignored but travels
+to the GPU box with the repo snapshot. One shared object holds the kernels
+(csrc/kernels.cu), the host runtime (csrc/host.cpp) and the C ABI
+(include/qrmc_gpu.h); CUDA runtime is linked statically, NCCL is dlopen'ed
+only for multi-GPU sessions.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT = PKG / "_lib" / "libqrmc_gpu.so"
+SOURCES = [CSRC / "kernels.cu", CSRC / "host.cpp"]
+HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", ROOT / "include" / "qrmc_gpu.h",
+           ROOT / "include" / "qrmc_normal_quantile.h"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def needs_build() -> bool:
+    if not OUT.exists():
+        return True
+    t = OUT.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in SOURCES + HEADERS + [Path(__file__)])
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not needs_build():
+        return OUT
+    OUT.parent.mkdir(parents=True, exist_ok=True)
+    tmp = OUT.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+           "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}",
+           *map(str, SOURCES), "-o", str(tmp), "-ldl"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr}")
+    if verbose and r.stderr:
+        print(r.stderr, file=sys.stderr)
+    tmp.replace(OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,921 @@
+// host.cpp -- host side of the B200 backward solver behind include/qrmc_gpu.h.
+//
+// Owns what the reference does on the host around its hot loop:
+//   * validation with the reference's rules and messages
+//     (ProblemSpec::validate sde.cpp:10-25, RunConfig::validate solver.cpp:23-35,
+//      SamplingMeasure ctor student.cpp:21-44)
+//   * multi-index set enumeration, bit-exact in order with
+//     proj/src/multi_index.cpp:96-173 (our own enumeration code)
+//   * the trie node program and packed coefficient layout the series kernel reads
+//   * the backward loop i = N-1..0 (solver.cpp:143-219) as a sequence of
+//     kernel launches captured once into a CUDA graph, with the per-step
+//     exchange of lane partials over NCCL when the solve spans several GPUs
+//   * mapping device error flags back to the reference's exception taxonomy
+// No computation of the solve happens here: there is no CPU fallback.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "qrmc_gpu.h"
+
+using namespace qrmc_dev;
+
+namespace {
+
+constexpr uint64_t kMaxIndices = 8'000'000;  // MultiIndexSet::kDefaultMaxIndices (multi_index.hpp:27)
+
+struct Failure {
+    qrmc_status status;
+    std::string msg;
+    int step = -1;
+};
+
+[[noreturn]] void fail(qrmc_status st, const std::string& msg) { throw Failure{st, msg}; }
+
+std::string fmt(const char* f, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, f);
+    std::vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(QRMC_ECUDA, fmt("%s: %s", what, cudaGetErrorString(e)));
+}
+
+void set_err(char* err, size_t len, const std::string& m) {
+    if (!err || !len) return;
+    std::strncpy(err, m.c_str(), len - 1);
+    err[len - 1] = 0;
+}
+
+template <class Fn>
+qrmc_status guarded(char* err, size_t err_len, Fn&& fn, qrmc_stats_t* stats = nullptr) {
+    try {
+        fn();
+        return QRMC_OK;
+    } catch (const Failure& f) {
+        set_err(err, err_len, f.msg);
+        if (stats) stats->error_step = f.step;
+        return f.status;
+    } catch (const std::bad_alloc&) {
+        set_err(err, err_len, "host allocation failed");
+        return QRMC_ECAPACITY;
+    } catch (const std::exception& e) {
+        set_err(err, err_len, e.what());
+        return QRMC_EINVAL;
+    }
+}
+
+// ------------------------------------------------------------------ Gamma
+struct Gamma {
+    int dim = 0;
+    int kind = 0;
+    std::vector<int32_t> rows;  // size x dim, lexicographic
+    std::vector<int> kmax;
+    int64_t size() const { return dim ? static_cast<int64_t>(rows.size() / dim) : 0; }
+};
+
+uint64_t binom_capped(uint64_t n, uint64_t k) {
+    // binomial(n, k), saturating above kMaxIndices (multi_index.cpp:17-27 semantics for the cap test)
+    if (k > n) return 0;
+    k = std::min(k, n - k);
+    long double r = 1;
+    for (uint64_t i = 1; i <= k; ++i) {
+        r = r * static_cast<long double>(n - k + i) / static_cast<long double>(i);
+        if (r > 1e30L) return UINT64_MAX;
+    }
+    return static_cast<uint64_t>(r + 0.5L);
+}
+
+Gamma build_gamma(int kind, int dim, const int32_t* degrees, int n_degrees) {
+    if (dim < 1) fail(QRMC_EINVAL, "multi-index set: dim must be >= 1");
+    if (!degrees || n_degrees < 1) fail(QRMC_EINVAL, "multi-index set: degrees missing");
+    Gamma g;
+    g.dim = dim;
+    g.kind = kind;
+    std::vector<int> k(static_cast<size_t>(dim), 0);
+    auto emit = [&] {
+        if (g.rows.size() / dim >= kMaxIndices) fail(QRMC_ECAPACITY, "index set exceeds index limit");
+        g.rows.insert(g.rows.end(), k.begin(), k.end());
+    };
+    if (kind == QRMC_GAMMA_FULL) {
+        if (n_degrees != 1 && n_degrees != dim) fail(QRMC_EINVAL, "full set: need dim degrees");
+        std::vector<int> K(static_cast<size_t>(dim));
+        uint64_t n = 1;
+        for (int l = 0; l < dim; ++l) {
+            K[l] = n_degrees == 1 ? degrees[0] : degrees[l];
+            if (K[l] < 0) fail(QRMC_EINVAL, "full set: degrees must be >= 0");
+            n *= static_cast<uint64_t>(K[l]) + 1;
+            if (n > kMaxIndices) fail(QRMC_ECAPACITY, "full set exceeds index limit");
+        }
+        g.rows.reserve(n * dim);
+        // odometer, rightmost coordinate fastest
+        for (;;) {
+            emit();
+            int l = dim - 1;
+            while (l >= 0 && k[l] == K[l]) k[l--] = 0;
+            if (l < 0) break;
+            ++k[l];
+        }
+    } else if (kind == QRMC_GAMMA_TOTAL) {
+        const int deg = degrees[0];
+        if (deg < 0) fail(QRMC_EINVAL, "total set: degree must be >= 0");
+        if (binom_capped(static_cast<uint64_t>(deg) + dim, dim) > kMaxIndices)
+            fail(QRMC_ECAPACITY, "total-degree set exceeds index limit");
+        // iterative depth-first walk: increments at the deepest level that still has budget
+        std::vector<int> used(static_cast<size_t>(dim) + 1, 0);  // used[l] = sum k[0..l-1]
+        for (;;) {
+            emit();
+            int l = dim - 1;
+            for (; l >= 0; --l) {
+                if (used[l] + k[l] + 1 <= deg) break;
+                k[l] = 0;
+            }
+            if (l < 0) break;
+            ++k[l];
+            for (int t = l + 1; t <= dim - 1; ++t) used[t] = used[t - 1] + k[t - 1];
+        }
+    } else if (kind == QRMC_GAMMA_HYPERBOLIC) {
+        const int deg = degrees[0];
+        if (deg < 1) fail(QRMC_EINVAL, "hyperbolic set: degree must be >= 1 (prod max(k_l,1) >= 1 always)");
+        std::vector<long long> pre(static_cast<size_t>(dim) + 1, 1);  // pre[l] = prod max(k,1) over 0..l-1
+        for (;;) {
+            emit();
+            int l = dim - 1;
+            for (; l >= 0; --l) {
+                if (pre[l] * std::max(k[l] + 1, 1) <= deg) break;
+                k[l] = 0;
+            }
+            if (l < 0) break;
+            ++k[l];
+            for (int t = l + 1; t <= dim; ++t) pre[t] = pre[t - 1] * std::max(k[t - 1], 1);
+        }
+    } else {
+        fail(QRMC_EINVAL, "unknown index set kind");
+    }
+    g.kmax.assign(static_cast<size_t>(dim), 0);
+    for (size_t i = 0; i < g.rows.size(); ++i) {
+        const int l = static_cast<int>(i % dim);
+        g.kmax[l] = std::max(g.kmax[l], g.rows[i]);
+    }
+    return g;
+}
+
+// Trie node program + packed layout (see series_eval in qrmc_device.cuh).
+struct Program {
+    std::vector<uint32_t> prog;
+    std::vector<int32_t> pack_pos;
+    std::vector<double> pack_scale;
+    int64_t kp = 0;
+};
+
+Program build_program(const Gamma& g) {
+    Program p;
+    const int d = g.dim;
+    const int64_t K = g.size();
+    p.pack_pos.resize(static_cast<size_t>(K));
+    p.pack_scale.resize(static_cast<size_t>(K));
+    int64_t pos = 0;
+    int64_t i = 0;
+    std::vector<int32_t> prev_prefix;
+    while (i < K) {
+        const int32_t* row = &g.rows[static_cast<size_t>(i * d)];
+        int64_t j = i;
+        auto same_prefix = [&](int64_t r) {
+            for (int l = 0; l < d - 1; ++l)
+                if (g.rows[static_cast<size_t>(r * d + l)] != row[l]) return false;
+            return true;
+        };
+        while (j < K && same_prefix(j)) {
+            if (g.rows[static_cast<size_t>(j * d + d - 1)] != j - i)
+                fail(QRMC_ELOGIC, "index set is not downward closed (leaf run)");
+            ++j;
+        }
+        const int64_t R = j - i;
+        int L = 0;
+        if (!prev_prefix.empty()) {
+            while (L < d - 1 && prev_prefix[L] == row[L]) ++L;
+            if (L >= d - 1 || row[L] != prev_prefix[L] + 1)
+                fail(QRMC_ELOGIC, "index set is not downward closed (node transition)");
+            for (int l = L + 1; l < d - 1; ++l)
+                if (row[l] != 0) fail(QRMC_ELOGIC, "index set is not downward closed (reset)");
+        }
+        if (L > 15 || R >= (int64_t{1} << 28)) fail(QRMC_ENOTIMPL, "index set too deep for the node program");
+        p.prog.push_back(static_cast<uint32_t>(L) | (static_cast<uint32_t>(R) << 4));
+        for (int64_t b = 0; b < R; ++b) {
+            const int32_t* r = &g.rows[static_cast<size_t>((i + b) * d)];
+            int nnz = 0;
+            for (int l = 0; l < d; ++l) nnz += r[l] != 0;
+            double s = std::ldexp(1.0, nnz / 2);
+            if (nnz & 1) s *= 1.4142135623730951;
+            p.pack_pos[static_cast<size_t>(i + b)] = static_cast<int32_t>(pos + b);
+            p.pack_scale[static_cast<size_t>(i + b)] = s;
+        }
+        pos += (R + 1) & ~int64_t{1};
+        prev_prefix.assign(row, row + std::max(d - 1, 0));
+        i = j;
+    }
+    p.kp = std::max<int64_t>(pos, 2);
+    return p;
+}
+
+// ------------------------------------------------------------------ problem / config
+ProblemDev to_device_problem(const qrmc_problem_t& p) {
+    // ProblemSpec::validate (sde.cpp:10-25)
+    if (p.dim < 1 || p.brownian_dim < 1) fail(QRMC_EINVAL, "ProblemSpec: dimensions must be >= 1");
+    if (!(p.horizon > 0.0)) fail(QRMC_EINVAL, "ProblemSpec: horizon must be positive");
+    const double consts[] = {p.growth_g, p.growth_exp_g, p.growth_f, p.growth_exp_f, p.lipschitz_f};
+    for (double c : consts)
+        if (!(c >= 0.0) || !std::isfinite(c))
+            fail(QRMC_EINVAL, "ProblemSpec: growth/Lipschitz constants must be finite and >= 0");
+    if (!(p.moment_ratio >= 1.0)) fail(QRMC_EINVAL, "ProblemSpec: moment_ratio must be >= 1");
+    if (p.terminal_kind < QRMC_TERMINAL_SIN_SUM || p.terminal_kind > QRMC_TERMINAL_NAN)
+        fail(QRMC_ENOTIMPL, "terminal kind has no device functor");
+    if (p.driver_kind < QRMC_DRIVER_ZERO || p.driver_kind > QRMC_DRIVER_SIN_BENCH)
+        fail(QRMC_ENOTIMPL, "driver kind has no device functor");
+    if (p.drift_kind != QRMC_DRIFT_ZERO && p.drift_kind != QRMC_DRIFT_CONST)
+        fail(QRMC_ENOTIMPL, "drift kind has no device functor");
+    if (p.diffusion_kind != QRMC_DIFFUSION_IDENTITY && p.diffusion_kind != QRMC_DIFFUSION_SCALAR)
+        fail(QRMC_ENOTIMPL, "diffusion kind has no device functor");
+    if (p.dim > kMaxDim) fail(QRMC_ENOTIMPL, fmt("dimension %d exceeds the device limit %d", p.dim, kMaxDim));
+    if (p.brownian_dim != p.dim)
+        fail(QRMC_ENOTIMPL, "device diffusions need brownian_dim == dim");
+    ProblemDev d{};
+    d.dim = p.dim;
+    d.bdim = p.brownian_dim;
+    d.horizon = p.horizon;
+    d.terminal_kind = p.terminal_kind;
+    d.driver_kind = p.driver_kind;
+    d.drift_kind = p.drift_kind;
+    d.diffusion_kind = p.diffusion_kind;
+    d.tp0 = p.terminal_params[0];
+    d.tp1 = p.terminal_params[1];
+    d.dp0 = p.driver_params[0];
+    d.dp1 = p.driver_params[1];
+    d.drift_c = p.drift_params[0];
+    d.sigma = p.diffusion_params[0];
+    // lstar_bound's x-independent factor, evaluated exactly as sde.cpp:28-29
+    d.lstar_base = p.moment_ratio * (p.growth_g + p.horizon * p.growth_f) *
+                   std::exp(p.moment_ratio * p.lipschitz_f * p.horizon);
+    d.eta = std::max(p.growth_exp_g, p.growth_exp_f);
+    d.state_bound = p.state_bound;
+    return d;
+}
+
+MeasureDev to_device_measure(const qrmc_config_t& c, int dim) {
+    // SamplingMeasure ctor (student.cpp:21-44)
+    if (!(c.mu > 0.0) || !std::isfinite(c.mu)) fail(QRMC_EINVAL, "SamplingMeasure: mu must be positive and finite");
+    if (dim < 1) fail(QRMC_EINVAL, "SamplingMeasure: dim must be >= 1");
+    if (dim > kMaxDim) fail(QRMC_ENOTIMPL, "dimension exceeds the device limit");
+    MeasureDev m{};
+    if (c.mu == 1.0)
+        m.form = 1;
+    else if (c.mu == 2.0)
+        m.form = 2;
+    else
+        fail(QRMC_ENOTIMPL, "general-mu Student measure has no device form (mu must be 1 or 2)");
+    for (int l = 0; l < dim; ++l) {
+        m.center[l] = c.center ? c.center[l] : 0.0;
+        if (!std::isfinite(m.center[l])) fail(QRMC_EINVAL, "SamplingMeasure: center must be finite");
+    }
+    return m;
+}
+
+void validate_config(const qrmc_config_t& c) {
+    // RunConfig::validate (solver.cpp:23-35)
+    if (c.steps < 1) fail(QRMC_EINVAL, "RunConfig: steps must be >= 1");
+    if (c.paths < 1) fail(QRMC_EINVAL, "RunConfig: paths must be >= 1");
+    if (!(c.damping >= 0.0) || !std::isfinite(c.damping)) fail(QRMC_EINVAL, "RunConfig: damping must be finite and >= 0");
+    if (c.workers < 0) fail(QRMC_EINVAL, "RunConfig: workers must be >= 0");
+    if (c.paths >= (int64_t{1} << kStepShift)) fail(QRMC_EINVAL, "RunConfig: paths exceeds the stream-id layout");
+    if (c.steps >= (1 << 22)) fail(QRMC_EINVAL, "RunConfig: steps exceeds the stream-id layout");
+    if (c.memory_mode != QRMC_MEMORY_STORE_CLOUD && c.memory_mode != QRMC_MEMORY_RECOMPUTE)
+        fail(QRMC_EINVAL, "unknown memory mode");
+}
+
+// ------------------------------------------------------------------ device buffers
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void upload(const T* h, size_t count, cudaStream_t st) {
+        cuda_check(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st), "H2D");
+    }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// ------------------------------------------------------------------ NCCL (loaded lazily)
+struct NcclApi {
+    void* handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            api.handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (api.handle) break;
+        }
+        if (!api.handle) return;
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.handle, "ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.handle, "ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.handle, "ncclCommDestroy"));
+        api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.handle, "ncclAllGather"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.handle, "ncclGetErrorString"));
+    });
+    if (!api.handle || !api.GetUniqueId || !api.CommInitRank || !api.AllGather)
+        fail(QRMC_ENCCL, "libnccl.so.2 could not be loaded");
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(QRMC_ENCCL, fmt("%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ session / plan
+struct qrmc_gpu_session {
+    int device = 0;
+    int rank = 0;
+    int world = 1;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+};
+
+struct qrmc_gpu_plan {
+    qrmc_gpu_session* session = nullptr;
+    bool owns_session = false;
+    Gamma gamma;
+    Program program;
+    StepArgs base{};
+    ProjArgs proj{};
+    int64_t K = 0;
+    int steps = 0;
+    int lanes_per_rank = kLanes;
+    DevBuf<uint32_t> d_prog;
+    DevBuf<int32_t> d_rows, d_pack_pos;
+    DevBuf<double> d_pack_scale, d_alpha, d_coef, d_partials, d_resp, d_cloud;
+    DevBuf<unsigned long long> d_counters;
+    DevBuf<int> d_flags;
+    cudaGraphExec_t graph = nullptr;
+    std::vector<cudaEvent_t> step_events;  // N+1 events bracketing the steps
+    int launches_per_run = 0;
+
+    ~qrmc_gpu_plan() {
+        if (graph) cudaGraphExecDestroy(graph);
+        for (auto e : step_events) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+std::unique_ptr<qrmc_gpu_session> make_session(int device, int rank, int world, const void* id) {
+    if (world < 1 || rank < 0 || rank >= world) fail(QRMC_EINVAL, "session: bad rank/world");
+    auto s = std::make_unique<qrmc_gpu_session>();
+    s->device = device;
+    s->rank = rank;
+    s->world = world;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (world > 1) {
+        if (!id) fail(QRMC_EINVAL, "session: world > 1 needs an NCCL unique id");
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof uid);
+        nccl_check(nccl().CommInitRank(&s->comm, world, uid, rank), "ncclCommInitRank");
+    }
+    return s;
+}
+
+void destroy_session(qrmc_gpu_session* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    if (s->comm) nccl().CommDestroy(s->comm);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+int current_device() {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    return dev;
+}
+
+// Enqueue the whole backward loop on st (captured into a graph when world == 1).
+void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
+    const int N = P.steps;
+    cuda_check(cudaMemsetAsync(P.d_counters.p, 0, 2 * sizeof(unsigned long long), st), "memset");
+    cuda_check(cudaMemsetAsync(P.d_flags.p, 0, sizeof(int), st), "memset");
+    // flags[1] = 0x7f7f7f7f: "no SimulationError step yet" for atomicMin
+    cuda_check(cudaMemsetAsync(P.d_flags.p + 1, 0x7f, sizeof(int), st), "memset");
+    if (with_events) cuda_check(cudaEventRecordWithFlags(P.step_events[0], st, cudaEventRecordExternal), "event");
+    const int world = P.session->world;
+    for (int i = N - 1; i >= 0; --i) {
+        StepArgs a = P.base;
+        a.step = i;
+        cuda_check(launch_responses(a, st), "k_responses");
+        ProjArgs pa = P.proj;
+        pa.partials = P.d_partials.p + static_cast<size_t>(P.session->rank) * P.lanes_per_rank * P.K;
+        cuda_check(launch_project(a, pa, st), "k_project");
+        if (world > 1) {
+            nccl_check(nccl().AllGather(pa.partials, P.d_partials.p, static_cast<size_t>(P.lanes_per_rank) * P.K,
+                                        ncclDouble, P.session->comm, st),
+                       "ncclAllGather");
+        }
+        FinishArgs f{};
+        f.all_partials = P.d_partials.p;
+        f.basis_size = P.K;
+        f.inv_m = 1.0 / static_cast<double>(P.base.paths);
+        f.coef_row = P.d_coef.p + static_cast<size_t>(i) * P.K;
+        f.pack_pos = P.d_pack_pos.p;
+        f.pack_scale = P.d_pack_scale.p;
+        cuda_check(launch_finish(a, f, st), "k_finish_step");
+        if (with_events) cuda_check(cudaEventRecordWithFlags(P.step_events[N - i], st, cudaEventRecordExternal), "event");
+    }
+}
+
+std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem_t& prob,
+                                         const qrmc_config_t& cfg) {
+    validate_config(cfg);
+    auto P = std::make_unique<qrmc_gpu_plan>();
+    P->session = s;
+    cuda_check(cudaSetDevice(s->device), "cudaSetDevice");
+    const ProblemDev pd = to_device_problem(prob);
+    P->gamma = build_gamma(cfg.gamma_kind, prob.dim, cfg.degrees, cfg.n_degrees);
+    if (P->gamma.dim != prob.dim) fail(QRMC_EINVAL, "RunConfig: gamma/measure dims must equal spec.dim");
+    const MeasureDev md = to_device_measure(cfg, prob.dim);
+    P->program = build_program(P->gamma);
+    P->K = P->gamma.size();
+    P->steps = cfg.steps;
+    const int d = prob.dim;
+    cudaStream_t st = s->stream;
+
+    // lane ownership: rank g owns lanes [g*lpr, min(256, (g+1)*lpr))
+    P->lanes_per_rank = (kLanes + s->world - 1) / s->world;
+    const int lo = s->rank * P->lanes_per_rank;
+    const int hi = std::min(kLanes, lo + P->lanes_per_rank);
+    const int64_t chunks = (cfg.paths + kChunk - 1) / kChunk;
+    int64_t n_owned = 0;
+    for (int lane = lo; lane < hi; ++lane)
+        for (int64_t c = lane; c < chunks; c += kLanes)
+            n_owned += std::min<int64_t>(kChunk, cfg.paths - c * kChunk);
+
+    // device tables
+    const Program& pg = P->program;
+    P->d_prog.alloc(pg.prog.size());
+    P->d_prog.upload(pg.prog.data(), pg.prog.size(), st);
+    P->d_rows.alloc(P->gamma.rows.size());
+    P->d_rows.upload(P->gamma.rows.data(), P->gamma.rows.size(), st);
+    P->d_pack_pos.alloc(pg.pack_pos.size());
+    P->d_pack_pos.upload(pg.pack_pos.data(), pg.pack_pos.size(), st);
+    P->d_pack_scale.alloc(pg.pack_scale.size());
+    P->d_pack_scale.upload(pg.pack_scale.data(), pg.pack_scale.size(), st);
+    P->d_alpha.alloc(static_cast<size_t>(cfg.steps) * pg.kp);
+    cuda_check(cudaMemsetAsync(P->d_alpha.p, 0, P->d_alpha.n * sizeof(double), st), "memset");
+    P->d_coef.alloc(static_cast<size_t>(cfg.steps) * P->K);
+    P->d_partials.alloc(static_cast<size_t>(P->lanes_per_rank) * s->world * P->K);
+    cuda_check(cudaMemsetAsync(P->d_partials.p, 0, P->d_partials.n * sizeof(double), st), "memset");
+    P->d_resp.alloc(static_cast<size_t>(std::max<int64_t>(n_owned, 1)));
+    if (cfg.memory_mode == QRMC_MEMORY_STORE_CLOUD)
+        P->d_cloud.alloc(static_cast<size_t>(std::max<int64_t>(n_owned, 1)) * d);
+    P->d_counters.alloc(2);
+    P->d_flags.alloc(2);
+
+    StepArgs& a = P->base;
+    a.prob = pd;
+    a.meas = md;
+    a.steps = cfg.steps;
+    a.step = cfg.steps - 1;
+    a.dt = prob.horizon / cfg.steps;
+    a.sqrt_dt = std::sqrt(a.dt);
+    a.q = cfg.damping;
+    a.seed = cfg.seed;
+    a.paths = cfg.paths;
+    a.lane_lo = lo;
+    a.owned_lanes = hi - lo;
+    a.n_owned = n_owned;
+    a.alpha_packed = P->d_alpha.p;
+    a.kp = pg.kp;
+    a.prog = P->d_prog.p;
+    a.n_runs = static_cast<int>(pg.prog.size());
+    a.resp = P->d_resp.p;
+    a.cloud = P->d_cloud.p;
+    a.counters = P->d_counters.p;
+    a.err_flags = P->d_flags.p;
+    a.abort_flag = P->d_flags.p;
+
+    ProjArgs& pa = P->proj;
+    pa.rows = P->d_rows.p;
+    int off = 0;
+    for (int l = 0; l < d; ++l) {
+        pa.offset[l] = off;
+        pa.kmax[l] = P->gamma.kmax[l];
+        off += P->gamma.kmax[l] + 1;
+    }
+    pa.table_len = off;
+    const size_t budget = 96 * 1024;
+    const size_t per_point = (static_cast<size_t>(off) + 1) * sizeof(double);
+    if (per_point > budget)
+        fail(QRMC_ENOTIMPL, fmt("per-point basis table of %d entries exceeds shared memory", off));
+    pa.batch = static_cast<int>(std::min<size_t>(64, budget / per_point));
+    pa.basis_size = P->K;
+
+    cuda_check(configure_project(d, project_smem_bytes(pa)), "k_project attributes");
+    P->step_events.resize(static_cast<size_t>(cfg.steps) + 1);
+    for (auto& e : P->step_events) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    P->launches_per_run = 3 * cfg.steps;
+
+    if (s->world == 1) {
+        cudaGraph_t g;
+        cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+        try {
+            enqueue_solve(*P, st, true);
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(st, &g), "capture end");
+        cuda_check(cudaGraphInstantiate(&P->graph, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+    }
+    cuda_check(cudaStreamSynchronize(st), "plan sync");
+    return P;
+}
+
+void run_plan(qrmc_gpu_plan& P, qrmc_stats_t* stats, double* step_wall) {
+    cudaStream_t st = P.session->stream;
+    cuda_check(cudaSetDevice(P.session->device), "cudaSetDevice");
+    if (P.graph)
+        cuda_check(cudaGraphLaunch(P.graph, st), "graph launch");
+    else
+        enqueue_solve(P, st, true);
+    cuda_check(cudaStreamSynchronize(st), "solve");
+    unsigned long long counters[2];
+    int flags[2];
+    cuda_check(cudaMemcpy(counters, P.d_counters.p, sizeof counters, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(flags, P.d_flags.p, sizeof flags, cudaMemcpyDeviceToHost), "D2H");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, P.step_events[0], P.step_events[P.steps]), "event time");
+    if (step_wall) {
+        for (int i = 0; i < P.steps; ++i) {
+            float t = 0.f;
+            cuda_check(cudaEventElapsedTime(&t, P.step_events[P.steps - 1 - i], P.step_events[P.steps - i]),
+                       "event time");
+            step_wall[i] = t * 1e-3;
+        }
+    }
+    if (stats) {
+        stats->applications = counters[0];
+        stats->clipped = counters[1];
+        stats->error_step = -1;
+        stats->kernel_launches = P.launches_per_run;
+        stats->device_seconds = ms * 1e-3;
+    }
+    if (flags[0] == QRMC_ESIM) {
+        Failure f{QRMC_ESIM, fmt("euler_step: state out of range at step %d", flags[1]), flags[1]};
+        throw f;
+    }
+    if (flags[0] == QRMC_ENUMERIC) fail(QRMC_ENUMERIC, "backward_solve: non-finite response or coefficient");
+}
+
+void download(qrmc_gpu_plan& P, double* coeffs, size_t len) {
+    const size_t need = static_cast<size_t>(P.steps) * P.K;
+    if (!coeffs || len < need) fail(QRMC_EINVAL, "coefficient buffer too small");
+    cuda_check(cudaMemcpy(coeffs, P.d_coef.p, need * sizeof(double), cudaMemcpyDeviceToHost), "D2H coeffs");
+}
+
+// A throwaway single-GPU context for the probe entry points.
+struct Scratch {
+    std::unique_ptr<qrmc_gpu_session, void (*)(qrmc_gpu_session*)> s{nullptr, destroy_session};
+    Scratch() { s.reset(make_session(current_device(), 0, 1, nullptr).release()); }
+};
+
+// Minimal StepArgs for probes that only need the problem and measure.
+StepArgs probe_args(const qrmc_problem_t* prob, const qrmc_config_t* cfg, int dim) {
+    StepArgs a{};
+    if (prob) a.prob = to_device_problem(*prob);
+    else a.prob.dim = dim;
+    a.meas = to_device_measure(*cfg, dim);
+    a.steps = cfg->steps;
+    const double horizon = prob ? prob->horizon : 1.0;
+    a.dt = horizon / std::max(cfg->steps, 1);
+    a.sqrt_dt = std::sqrt(a.dt);
+    a.q = cfg->damping;
+    a.seed = cfg->seed;
+    a.paths = cfg->paths;
+    return a;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+qrmc_status qrmc_problem_sin_bench(int32_t dim, double kappa, double lambda, double horizon,
+                                   qrmc_problem_t* out) {
+    if (!out || dim < 1) return QRMC_EINVAL;
+    if (!(horizon > 0.0)) return QRMC_EINVAL;
+    std::memset(out, 0, sizeof *out);
+    const double lam = lambda > 0.0 ? lambda : 1.0 / std::sqrt(static_cast<double>(dim));
+    out->dim = dim;
+    out->brownian_dim = dim;
+    out->horizon = horizon;
+    out->terminal_kind = QRMC_TERMINAL_SIN_SUM;
+    out->driver_kind = QRMC_DRIVER_SIN_BENCH;
+    out->drift_kind = QRMC_DRIFT_ZERO;
+    out->diffusion_kind = QRMC_DIFFUSION_IDENTITY;
+    out->terminal_params[0] = out->driver_params[0] = kappa;
+    out->terminal_params[1] = out->driver_params[1] = lam;
+    out->growth_g = 2.0 + kappa;
+    out->growth_f = 1.0;
+    out->lipschitz_f = 2.0;
+    out->moment_ratio = 1.0;
+    out->state_bound = 1e15;
+    return QRMC_OK;
+}
+
+int64_t qrmc_gpu_gamma_size(int32_t kind, int32_t dim, const int32_t* degrees, int32_t n_degrees) {
+    int64_t n = 0;
+    const qrmc_status st = guarded(nullptr, 0, [&] { n = build_gamma(kind, dim, degrees, n_degrees).size(); });
+    return st == QRMC_OK ? n : -static_cast<int64_t>(st);
+}
+
+qrmc_status qrmc_gpu_gamma_indices(int32_t kind, int32_t dim, const int32_t* degrees, int32_t n_degrees,
+                                   int32_t* out, size_t out_len, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        const Gamma g = build_gamma(kind, dim, degrees, n_degrees);
+        if (!out || out_len < g.rows.size()) fail(QRMC_EINVAL, "output buffer too small");
+        std::memcpy(out, g.rows.data(), g.rows.size() * sizeof(int32_t));
+    });
+}
+
+qrmc_status qrmc_gpu_nccl_unique_id(void* out128, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        ncclUniqueId id;
+        nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out128, &id, sizeof id);
+    });
+}
+
+qrmc_status qrmc_gpu_session_create(int32_t device, int32_t rank, int32_t world, const void* nccl_unique_id,
+                                    qrmc_gpu_session_t** out, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!out) fail(QRMC_EINVAL, "session: null output");
+        *out = make_session(device, rank, world, nccl_unique_id).release();
+    });
+}
+
+void qrmc_gpu_session_destroy(qrmc_gpu_session_t* s) { destroy_session(s); }
+
+qrmc_status qrmc_gpu_plan_create(qrmc_gpu_session_t* session, const qrmc_problem_t* problem,
+                                 const qrmc_config_t* config, qrmc_gpu_plan_t** out, char* err,
+                                 size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!problem || !config || !out) fail(QRMC_EINVAL, "plan: null argument");
+        bool owns = false;
+        if (!session) {
+            session = make_session(current_device(), 0, 1, nullptr).release();
+            owns = true;
+        }
+        try {
+            auto P = make_plan(session, *problem, *config);
+            P->owns_session = owns;
+            *out = P.release();
+        } catch (...) {
+            if (owns) destroy_session(session);
+            throw;
+        }
+    });
+}
+
+qrmc_status qrmc_gpu_plan_run(qrmc_gpu_plan_t* plan, qrmc_stats_t* stats, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!plan) fail(QRMC_EINVAL, "plan: null");
+        run_plan(*plan, stats, nullptr);
+    }, stats);
+}
+
+qrmc_status qrmc_gpu_plan_download(qrmc_gpu_plan_t* plan, double* coeffs, size_t coeffs_len, char* err,
+                                   size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!plan) fail(QRMC_EINVAL, "plan: null");
+        cuda_check(cudaSetDevice(plan->session->device), "cudaSetDevice");
+        download(*plan, coeffs, coeffs_len);
+    });
+}
+
+int64_t qrmc_gpu_plan_basis_size(const qrmc_gpu_plan_t* plan) { return plan ? plan->K : -1; }
+
+void* qrmc_gpu_plan_stream(const qrmc_gpu_plan_t* plan) {
+    return plan ? static_cast<void*>(plan->session->stream) : nullptr;
+}
+
+void qrmc_gpu_plan_destroy(qrmc_gpu_plan_t* plan) {
+    if (!plan) return;
+    qrmc_gpu_session* s = plan->owns_session ? plan->session : nullptr;
+    cudaSetDevice(plan->session->device);
+    delete plan;
+    destroy_session(s);
+}
+
+qrmc_status qrmc_gpu_backward_solve(qrmc_gpu_session_t* session, const qrmc_problem_t* problem,
+                                    const qrmc_config_t* config, double* coeffs, size_t coeffs_len,
+                                    double* step_wall_seconds, qrmc_stats_t* stats, char* err,
+                                    size_t err_len) {
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->error_step = -1;
+    }
+    return guarded(err, err_len, [&] {
+        if (!problem || !config) fail(QRMC_EINVAL, "backward_solve: null argument");
+        std::unique_ptr<qrmc_gpu_session, void (*)(qrmc_gpu_session*)> own(nullptr, destroy_session);
+        if (!session) {
+            own.reset(make_session(current_device(), 0, 1, nullptr).release());
+            session = own.get();
+        }
+        // validate the output buffer before any device work
+        const Gamma g = build_gamma(config->gamma_kind, problem->dim, config->degrees, config->n_degrees);
+        if (!coeffs || coeffs_len < static_cast<size_t>(g.size()) * static_cast<size_t>(std::max(config->steps, 0)))
+            fail(QRMC_EINVAL, "coefficient buffer too small");
+        auto P = make_plan(session, *problem, *config);
+        run_plan(*P, stats, step_wall_seconds);
+        download(*P, coeffs, coeffs_len);
+    }, stats);
+}
+
+qrmc_status qrmc_gpu_evaluate(const qrmc_config_t* config, int32_t dim, const double* coeffs_step,
+                              const double* x, int64_t n, double* out, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!config || !coeffs_step || (!x && n) || (!out && n)) fail(QRMC_EINVAL, "evaluate: null argument");
+        Scratch sc;
+        cudaStream_t st = sc.s->stream;
+        const Gamma g = build_gamma(config->gamma_kind, dim, config->degrees, config->n_degrees);
+        const Program pg = build_program(g);
+        StepArgs a = probe_args(nullptr, config, dim);
+        std::vector<double> packed(static_cast<size_t>(pg.kp), 0.0);
+        for (int64_t k = 0; k < g.size(); ++k) packed[pg.pack_pos[k]] = coeffs_step[k] * pg.pack_scale[k];
+        DevBuf<double> d_alpha(packed.size()), d_x(static_cast<size_t>(std::max<int64_t>(n, 1)) * dim),
+            d_out(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        DevBuf<uint32_t> d_prog(pg.prog.size());
+        d_alpha.upload(packed.data(), packed.size(), st);
+        d_prog.upload(pg.prog.data(), pg.prog.size(), st);
+        if (n) d_x.upload(x, static_cast<size_t>(n) * dim, st);
+        a.prog = d_prog.p;
+        a.n_runs = static_cast<int>(pg.prog.size());
+        if (n) cuda_check(launch_eval_points(a, d_alpha.p, d_x.p, n, config->damping, 1, d_out.p, st), "k_eval_points");
+        cuda_check(cudaStreamSynchronize(st), "evaluate");
+        if (n) cuda_check(cudaMemcpy(out, d_out.p, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+qrmc_status qrmc_gpu_mse_metrics(const qrmc_config_t* config, int32_t dim, double kappa, double lambda,
+                                 double horizon, const double* coeffs, uint64_t eval_seed,
+                                 int32_t eval_points, double* out6, double* step_sq, char* err,
+                                 size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!config || !coeffs || !out6) fail(QRMC_EINVAL, "mse_metrics: null argument");
+        if (eval_points < 1) fail(QRMC_EINVAL, "mse_metrics: eval_points must be >= 1");
+        Scratch sc;
+        cudaStream_t st = sc.s->stream;
+        const Gamma g = build_gamma(config->gamma_kind, dim, config->degrees, config->n_degrees);
+        const Program pg = build_program(g);
+        qrmc_problem_t prob{};
+        qrmc_problem_sin_bench(dim, kappa, lambda, horizon, &prob);
+        StepArgs a = probe_args(&prob, config, dim);
+        const int N = config->steps;
+        std::vector<double> packed(static_cast<size_t>(pg.kp) * N, 0.0);
+        for (int i = 0; i < N; ++i)
+            for (int64_t k = 0; k < g.size(); ++k)
+                packed[static_cast<size_t>(i) * pg.kp + pg.pack_pos[k]] = coeffs[static_cast<size_t>(i) * g.size() + k] * pg.pack_scale[k];
+        DevBuf<double> d_alpha(packed.size()), d_sq(static_cast<size_t>(N) * eval_points),
+            d_squ(static_cast<size_t>(N) * eval_points);
+        DevBuf<uint32_t> d_prog(pg.prog.size());
+        d_alpha.upload(packed.data(), packed.size(), st);
+        d_prog.upload(pg.prog.data(), pg.prog.size(), st);
+        a.prog = d_prog.p;
+        a.n_runs = static_cast<int>(pg.prog.size());
+        a.alpha_packed = d_alpha.p;
+        a.kp = pg.kp;
+        const double lam = prob.terminal_params[1];
+        cuda_check(launch_mse(a, kappa, lam, horizon, eval_seed, eval_points, d_sq.p, d_squ.p, st), "k_mse");
+        std::vector<double> sq(d_sq.n), squ(d_squ.n);
+        cuda_check(cudaStreamSynchronize(st), "mse");
+        cuda_check(cudaMemcpy(sq.data(), d_sq.p, sq.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(squ.data(), d_squ.p, squ.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        // metrics_from_squared_errors (benchmark.cpp:69-84), in the reference's order
+        double mx = 0.0, tot = 0.0, mxu = 0.0, totu = 0.0;
+        for (int i = 0; i < N; ++i) {
+            double s = 0.0, su = 0.0;
+            for (int m = 0; m < eval_points; ++m) {
+                s += sq[static_cast<size_t>(i) * eval_points + m];
+                su += squ[static_cast<size_t>(i) * eval_points + m];
+            }
+            mx = std::max(mx, s);
+            tot += s;
+            mxu = std::max(mxu, su);
+            totu += su;
+            if (step_sq) step_sq[i] = s;
+        }
+        const double nn = eval_points, steps = N;
+        out6[0] = std::log(mx / nn);
+        out6[1] = std::log(tot / (steps * nn));
+        out6[2] = std::log(mxu / nn);
+        out6[3] = std::log(totu / (steps * nn));
+        out6[4] = out6[5] = 0.0;
+    });
+}
+
+qrmc_status qrmc_gpu_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out, char* err,
+                            size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (n <= 0) return;
+        Scratch sc;
+        cudaStream_t st = sc.s->stream;
+        DevBuf<uint32_t> d_ctr(static_cast<size_t>(n) * 4), d_key(static_cast<size_t>(n) * 2), d_out(static_cast<size_t>(n) * 4);
+        d_ctr.upload(ctr, d_ctr.n, st);
+        d_key.upload(key, d_key.n, st);
+        cuda_check(launch_philox(d_ctr.p, d_key.p, n, d_out.p, st), "k_philox");
+        cuda_check(cudaStreamSynchronize(st), "philox");
+        cuda_check(cudaMemcpy(out, d_out.p, d_out.n * sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+qrmc_status qrmc_gpu_stream_draws(uint64_t seed, const uint64_t* stream_ids, int64_t n_streams, int32_t n_draws,
+                                  int32_t kind, void* out, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (n_streams <= 0 || n_draws <= 0) return;
+        if (kind < 0 || kind > 2) fail(QRMC_EINVAL, "stream_draws: kind must be 0, 1 or 2");
+        Scratch sc;
+        cudaStream_t st = sc.s->stream;
+        DevBuf<uint64_t> d_sid(static_cast<size_t>(n_streams)), d_out(static_cast<size_t>(n_streams) * n_draws);
+        d_sid.upload(stream_ids, d_sid.n, st);
+        cuda_check(launch_stream_draws(seed, d_sid.p, n_streams, n_draws, kind, d_out.p, st), "k_stream_draws");
+        cuda_check(cudaStreamSynchronize(st), "draws");
+        cuda_check(cudaMemcpy(out, d_out.p, d_out.n * sizeof(uint64_t), cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+qrmc_status qrmc_gpu_cloud_paths(const qrmc_problem_t* problem, const qrmc_config_t* config, int32_t step,
+                                 int64_t first, int64_t n, double* out, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!problem || !config) fail(QRMC_EINVAL, "cloud_paths: null argument");
+        if (step < 0 || step > config->steps) fail(QRMC_EINVAL, "cloud_paths: step out of range");
+        if (n <= 0) return;
+        Scratch sc;
+        cudaStream_t st = sc.s->stream;
+        StepArgs a = probe_args(problem, config, problem->dim);
+        a.step = step;
+        const size_t len = static_cast<size_t>(config->steps - step + 1) * problem->dim;
+        DevBuf<double> d_out(static_cast<size_t>(n) * len);
+        DevBuf<int> d_bad(1);
+        cuda_check(cudaMemsetAsync(d_bad.p, 0, sizeof(int), st), "memset");
+        cuda_check(launch_cloud_paths(a, first, n, d_out.p, d_bad.p, st), "k_cloud_paths");
+        cuda_check(cudaStreamSynchronize(st), "paths");
+        int bad = 0;
+        cuda_check(cudaMemcpy(&bad, d_bad.p, sizeof bad, cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(out, d_out.p, d_out.n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        if (bad) {
+            Failure f{QRMC_ESIM, fmt("euler_step: state out of range at step %d", bad), bad};
+            throw f;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,374 @@
+// kernels.cu -- the sm_100a kernels of one backward step and their launchers.
+//
+// One backward step i of backward_solve (proj/src/solver.cpp:143-219) is
+//   K1 k_responses    phase 1: per path, draw X_i ~ nu, Euler to N, evaluate
+//                     every future series alpha_{j+1} at X_{j+1}, truncate,
+//                     accumulate the driver, emit S_m (solver.cpp:147-177)
+//   K2 k_project      phase 2: per lane, acc[lane][k] = sum_m S_m phi_k(X_i^m)
+//                     in the reference's lane/chunk order (solver.cpp:180-199)
+//   K3 k_finish_step  coeffs[k] = (sum_{lane=0..255} acc[lane][k]) * (1/M),
+//                     finiteness check, and the packed alpha' row the next
+//                     steps' K1 reads (solver.cpp:201-213)
+// plus the probes behind the C ABI's replay entry points.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "qrmc_device.cuh"
+
+namespace qrmc_dev {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ int64_t owned_to_path(const StepArgs& a, int64_t q) {
+    // owned index q -> global path m: owned chunk cq = q / 1024 is (round r,
+    // lane lo + cq % owned_lanes), chunk c = 256 r + lane (LaneLayout::for_lane,
+    // parallel.hpp:28-35, restricted to this rank's lanes).
+    const int64_t cq = q / kChunk;
+    const int64_t r = cq / a.owned_lanes;
+    const int64_t lane = a.lane_lo + cq % a.owned_lanes;
+    return (r * kLanes + lane) * kChunk + q % kChunk;
+}
+
+__device__ __forceinline__ void record_error(int* flags, int kind, int step) {
+    // flags[0] = first error kind (QRMC_ESIM / QRMC_ENUMERIC), flags[1] = min sim step
+    atomicCAS(flags, 0, kind);
+    if (kind == QRMC_ESIM) atomicMin(flags + 1, step);
+}
+
+__device__ __forceinline__ void sample_start(const MeasureDev& m, int d, Stream& s, double* x) {
+    for (int l = 0; l < d; ++l) x[l] = measure_inv_cdf(m, s.next_uniform(), l);
+}
+
+template <int D>
+__device__ __forceinline__ double eval_at(const StepArgs& a, const double* alpha_row, const double* x) {
+    double c1[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) c1[l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, x[l], l)));
+    return series_eval<D>(alpha_row, a.prog, a.n_runs, c1);
+}
+
+// ---------------------------------------------------------------- K1
+template <int D>
+__global__ void __launch_bounds__(128) k_responses(const StepArgs a) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint32_t apps = 0, clipped = 0;
+    if (q < a.n_owned && !*a.abort_flag) {
+        const int64_t m = owned_to_path(a, q);
+        Stream s(a.seed, sid_training(a.step, static_cast<uint64_t>(m)));
+        double x0[D], xj[D], xn[D];
+        sample_start(a.meas, D, s, x0);
+#pragma unroll
+        for (int l = 0; l < D; ++l) xj[l] = x0[l];
+        double driver_sum = 0.0;
+        int bad = 0;
+        for (int j = a.step; j < a.steps; ++j) {
+#pragma unroll
+            for (int l = 0; l < D; ++l) xn[l] = xj[l];
+            const int b = euler_step(a.prob, xn, a.sqrt_dt, a.dt, s, j);
+            if (b) {
+                bad = b;
+                break;
+            }
+            double y_next;
+            if (j + 1 == a.steps) {
+                y_next = terminal(a.prob, xn);  // exact initialisation (solver.cpp:69-72)
+            } else {
+                const double* row = a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp;
+                y_next = DMUL(eval_at<D>(a, row, xn), damping_weight(xn, D, a.q));
+            }
+            const double c = truncate_soft(y_next, lstar(a.prob, xn));
+            ++apps;
+            if (c != y_next) ++clipped;
+            driver_sum = DADD(driver_sum, driver(a.prob, DMUL(static_cast<double>(j), a.dt), xj, c));
+#pragma unroll
+            for (int l = 0; l < D; ++l) xj[l] = xn[l];
+        }
+        if (bad) {
+            record_error(a.err_flags, QRMC_ESIM, bad);
+        } else {
+            const double term = terminal(a.prob, xj);
+            const double v = DDIV(DADD(term, DMUL(a.dt, driver_sum)), damping_weight(x0, D, a.q));
+            if (!isfinite(v)) record_error(a.err_flags, QRMC_ENUMERIC, 0);
+            a.resp[q] = v;
+            if (a.cloud) {
+#pragma unroll
+                for (int l = 0; l < D; ++l) a.cloud[l * a.n_owned + q] = x0[l];
+            }
+        }
+    }
+    // truncation counters: warp-aggregate then one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) {
+        apps += __shfl_down_sync(0xffffffffu, apps, o);
+        clipped += __shfl_down_sync(0xffffffffu, clipped, o);
+    }
+    if ((threadIdx.x & 31) == 0 && apps) {
+        atomicAdd(a.counters, static_cast<unsigned long long>(apps));
+        if (clipped) atomicAdd(a.counters + 1, static_cast<unsigned long long>(clipped));
+    }
+}
+
+// ---------------------------------------------------------------- K2
+// CTA (term tile, owned lane). Each thread owns kTermsPerThread terms and sums
+// S_m * phi_k(X_m) over the lane's paths in ascending m -- the reference's
+// per-lane order -- with the reference's own table values and product order
+// (cosine_basis.cpp:71-97), so the lane partial is the reference's bit pattern
+// whenever S_m and the cosine values agree.
+constexpr int kProjThreads = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, const ProjArgs p) {
+    extern __shared__ double smem[];
+    double* tab = smem;                          // [batch][table_len]
+    double* sv = smem + p.batch * p.table_len;   // [batch]
+    const int lane_rel = blockIdx.y;
+    const int lane = a.lane_lo + lane_rel;
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kProjThreads * kTermsPerThread;
+
+    int idx[kTermsPerThread][D];
+    bool live[kTermsPerThread];
+    double acc[kTermsPerThread];
+#pragma unroll
+    for (int t = 0; t < kTermsPerThread; ++t) {
+        const int64_t k = k0 + t * kProjThreads + threadIdx.x;
+        live[t] = k < p.basis_size;
+        acc[t] = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) idx[t][l] = live[t] ? p.offset[l] + p.rows[k * D + l] : 0;
+    }
+
+    const int64_t chunks_total = (a.paths + kChunk - 1) / kChunk;
+    for (int64_t c = lane; c < chunks_total; c += kLanes) {
+        const int64_t r = c / kLanes;
+        const int64_t q_chunk = (r * a.owned_lanes + lane_rel) * kChunk;  // owned index of the chunk
+        const int64_t m_chunk = c * kChunk;
+        const int64_t rem = a.paths - m_chunk;
+        const int len = static_cast<int>(rem < kChunk ? rem : kChunk);
+        for (int base = 0; base < len; base += p.batch) {
+            const int nb = min(p.batch, len - base);
+            __syncthreads();
+            // tables: one (point, coordinate) recurrence per thread
+            for (int task = threadIdx.x; task < nb * D; task += kProjThreads) {
+                const int pt = task / D, l = task % D;
+                const int64_t q = q_chunk + base + pt;
+                double xl;
+                if (a.cloud) {
+                    xl = a.cloud[l * a.n_owned + q];
+                } else {
+                    // recompute-from-seeds (solver.cpp:187-193): regenerate X_i
+                    Stream s(a.seed, sid_training(a.step, static_cast<uint64_t>(m_chunk + base + pt)));
+                    double u = 0.0;
+                    for (int ll = 0; ll <= l; ++ll) u = s.next_uniform();
+                    xl = measure_inv_cdf(a.meas, u, l);
+                }
+                const double c1 = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xl, l)));
+                double* t = tab + pt * p.table_len + p.offset[l];
+                const int kmax = p.kmax[l];
+                t[0] = 1.0;
+                if (kmax >= 1) {
+                    const double sqrt2 = 1.4142135623730951;
+                    double prev = 1.0, cur = c1;
+                    t[1] = DMUL(sqrt2, c1);
+                    const double two_c1 = DMUL(2.0, c1);
+                    for (int k = 2; k <= kmax; ++k) {
+                        const double nx = DSUB(DMUL(two_c1, cur), prev);
+                        prev = cur;
+                        cur = nx;
+                        t[k] = DMUL(sqrt2, nx);
+                    }
+                }
+                if (l == 0) sv[pt] = a.resp[q];
+            }
+            __syncthreads();
+            for (int pt = 0; pt < nb; ++pt) {
+                const double* t = tab + pt * p.table_len;
+                const double s_m = sv[pt];
+#pragma unroll
+                for (int tt = 0; tt < kTermsPerThread; ++tt) {
+                    double prod = 1.0;
+#pragma unroll
+                    for (int l = 0; l < D; ++l) prod = DMUL(prod, t[idx[tt][l]]);
+                    acc[tt] = DADD(acc[tt], DMUL(s_m, prod));
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kTermsPerThread; ++t) {
+        const int64_t k = k0 + t * kProjThreads + threadIdx.x;
+        if (live[t]) p.partials[static_cast<int64_t>(lane_rel) * p.basis_size + k] = acc[t];
+    }
+}
+
+// ---------------------------------------------------------------- K3
+__global__ void k_finish_step(const StepArgs a, const FinishArgs f) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= f.basis_size) return;
+    double sum = 0.0;
+    for (int lane = 0; lane < kLanes; ++lane) sum = DADD(sum, f.all_partials[static_cast<int64_t>(lane) * f.basis_size + k]);
+    const double v = DMUL(sum, f.inv_m);
+    if (!isfinite(v)) record_error(a.err_flags, QRMC_ENUMERIC, 0);
+    f.coef_row[k] = v;
+    a.alpha_packed[static_cast<int64_t>(a.step) * a.kp + f.pack_pos[k]] = DMUL(v, f.pack_scale[k]);
+}
+
+// ---------------------------------------------------------------- probes
+__global__ void k_philox(const uint4* ctr, const uint2* key, int64_t n, uint4* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = philox4x32_10(ctr[i], key[i]);
+}
+
+__global__ void k_stream_draws(uint64_t seed, const uint64_t* sids, int64_t n, int n_draws, int kind,
+                               void* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Stream s(seed, sids[i]);
+    for (int k = 0; k < n_draws; ++k) {
+        const int64_t at = i * n_draws + k;
+        if (kind == 0)
+            static_cast<uint64_t*>(out)[at] = s.next_u64();
+        else if (kind == 1)
+            static_cast<double*>(out)[at] = s.next_uniform();
+        else
+            static_cast<double*>(out)[at] = s.next_normal();
+    }
+}
+
+__global__ void k_cloud_paths(const StepArgs a, int64_t first, int64_t n, double* out, int* bad_out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int d = a.prob.dim;
+    const int64_t len = static_cast<int64_t>(a.steps - a.step + 1) * d;
+    double* path = out + r * len;
+    Stream s(a.seed, sid_training(a.step, static_cast<uint64_t>(first + r)));
+    double x[kMaxDim];
+    sample_start(a.meas, d, s, x);
+    for (int l = 0; l < d; ++l) path[l] = x[l];
+    for (int j = a.step; j < a.steps; ++j) {
+        const int b = euler_step(a.prob, x, a.sqrt_dt, a.dt, s, j);
+        if (b) {
+            atomicMax(bad_out, b);
+            return;
+        }
+        for (int l = 0; l < d; ++l) path[(j + 1 - a.step) * d + l] = x[l];
+    }
+}
+
+template <int D>
+__global__ void k_eval_points(const StepArgs a, const double* alpha_row, const double* x, int64_t n,
+                              double q, int with_weight, double* out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double p[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) p[l] = x[r * D + l];
+    const double y = eval_at<D>(a, alpha_row, p);
+    out[r] = with_weight ? DMUL(y, damping_weight(p, D, q)) : y;
+}
+
+// mse_metrics (benchmark.cpp:86-151): per (step i, point m) squared errors of
+// the damped series against exact_solution/weight (benchmark.cpp:20-28).
+template <int D>
+__global__ void k_mse(const StepArgs a, double kappa, double lam, double horizon, uint64_t eval_seed,
+                      int eval_points, double* sq, double* sq_u) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    if (r >= eval_points) return;
+    Stream s(eval_seed, sid_evaluation(i, static_cast<uint64_t>(r)));
+    double p[D];
+    sample_start(a.meas, D, s, p);
+    const double w = damping_weight(p, D, a.q);
+    const double approx = eval_at<D>(a, a.alpha_packed + static_cast<int64_t>(i) * a.kp, p);
+    const double t = DMUL(static_cast<double>(i), a.dt);
+    const double e_exp = exp(DDIV(DMUL(DMUL(DMUL(lam, lam), static_cast<double>(D)), DSUB(t, horizon)), 2.0));
+    const double truth = DADD(DADD(1.0, kappa), DMUL(sin(DMUL(lam, sum_of(p, D))), e_exp));
+    const double e = DSUB(approx, DDIV(truth, w));
+    sq[static_cast<int64_t>(i) * eval_points + r] = DMUL(e, e);
+    sq_u[static_cast<int64_t>(i) * eval_points + r] = DMUL(DMUL(DMUL(e, e), w), w);
+}
+
+// ---------------------------------------------------------------- dispatch
+#define QRMC_DISPATCH_D(dim, CALL)                  \
+    switch (dim) {                                  \
+        case 1: { constexpr int D = 1; CALL; } break; \
+        case 2: { constexpr int D = 2; CALL; } break; \
+        case 3: { constexpr int D = 3; CALL; } break; \
+        case 4: { constexpr int D = 4; CALL; } break; \
+        case 5: { constexpr int D = 5; CALL; } break; \
+        case 6: { constexpr int D = 6; CALL; } break; \
+        case 7: { constexpr int D = 7; CALL; } break; \
+        case 8: { constexpr int D = 8; CALL; } break; \
+        default: return cudaErrorInvalidValue;      \
+    }
+
+cudaError_t launch_responses(const StepArgs& a, cudaStream_t st) {
+    if (a.n_owned == 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>((a.n_owned + 127) / 128);
+    QRMC_DISPATCH_D(a.prob.dim, (k_responses<D><<<blocks, 128, 0, st>>>(a)));
+    return cudaGetLastError();
+}
+
+size_t project_smem_bytes(const ProjArgs& p) {
+    return (static_cast<size_t>(p.batch) * p.table_len + p.batch) * sizeof(double);
+}
+
+cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st) {
+    const unsigned tiles = static_cast<unsigned>((p.basis_size + kProjThreads * kTermsPerThread - 1) /
+                                                 (kProjThreads * kTermsPerThread));
+    const dim3 grid(tiles, static_cast<unsigned>(a.owned_lanes));
+    const size_t smem = project_smem_bytes(p);
+    QRMC_DISPATCH_D(a.prob.dim, (k_project<D><<<grid, kProjThreads, smem, st>>>(a, p)));
+    return cudaGetLastError();
+}
+
+cudaError_t configure_project(int dim, size_t smem) {
+    cudaError_t e = cudaSuccess;
+    QRMC_DISPATCH_D(dim, (e = cudaFuncSetAttribute(k_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem))));
+    return e;
+}
+
+cudaError_t launch_finish(const StepArgs& a, const FinishArgs& f, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((f.basis_size + 255) / 256);
+    k_finish_step<<<blocks, 256, 0, st>>>(a, f);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out,
+                          cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+    k_philox<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(ctr),
+                                     reinterpret_cast<const uint2*>(key), n,
+                                     reinterpret_cast<uint4*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stream_draws(uint64_t seed, const uint64_t* sids, int64_t n, int n_draws, int kind,
+                                void* out, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((n + 127) / 128);
+    k_stream_draws<<<blocks, 128, 0, st>>>(seed, sids, n, n_draws, kind, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cloud_paths(const StepArgs& a, int64_t first, int64_t n, double* out, int* bad,
+                               cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((n + 127) / 128);
+    k_cloud_paths<<<blocks, 128, 0, st>>>(a, first, n, out, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_points(const StepArgs& a, const double* alpha_row, const double* x, int64_t n,
+                               double q, int with_weight, double* out, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((n + 127) / 128);
+    QRMC_DISPATCH_D(a.prob.dim, (k_eval_points<D><<<blocks, 128, 0, st>>>(a, alpha_row, x, n, q, with_weight, out)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mse(const StepArgs& a, double kappa, double lam, double horizon, uint64_t eval_seed,
+                       int eval_points, double* sq, double* sq_u, cudaStream_t st) {
+    const dim3 grid(static_cast<unsigned>((eval_points + 127) / 128), static_cast<unsigned>(a.steps));
+    QRMC_DISPATCH_D(a.prob.dim, (k_mse<D><<<grid, 128, 0, st>>>(a, kappa, lam, horizon, eval_seed, eval_points, sq, sq_u)));
+    return cudaGetLastError();
+}
+
+}  // namespace qrmc_dev

@@ -1,0 +1,278 @@
+// qrmc_device.cuh -- device-side building blocks of the backward solver.
+//
+// Every function here is the sm_100a counterpart of one reference routine
+// (file:line cited per function). The replay-critical arithmetic (random
+// draws, sampling, Euler, truncation, weights, functors) is spelled with
+// explicit round-to-nearest intrinsics so ptxas cannot contract it into FMAs:
+// the reference's numerics contain no FMA, and with this the
+// device reproduces the reference's Philox words, uniforms and mu=2 starts
+// bit for bit and its Gaussians and Euler paths to the last ulp of log().
+// The series evaluation (the FLOP-dominant part) is the one place that uses
+// FMAs and a re-associated (sum-factorised) order; its deviation is covered
+// by the stated FP64 tolerance ("Parity").
+#pragma once
+
+#include <cstdint>
+
+#include "qrmc_gpu.h"
+#include "qrmc_normal_quantile.h"
+#include "qrmc_types.h"
+
+namespace qrmc_dev {
+
+
+#define DMUL(a, b) __dmul_rn((a), (b))
+#define DADD(a, b) __dadd_rn((a), (b))
+#define DSUB(a, b) __dsub_rn((a), (b))
+#define DDIV(a, b) __ddiv_rn((a), (b))
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (proj/src/rng.cpp:9-40): multipliers 0xD2511F53/0xCD9E8D57,
+// Weyl increments 0x9E3779B9/0xBB67AE85, key bumped before rounds 1..9.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) {
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+// RngStream (rng.hpp:26-65): key = seed, counter = (block lo, block hi,
+// stream id lo, stream id hi); each block yields two u64 draws
+// (o1<<32|o0), (o3<<32|o2).
+struct Stream {
+    uint2 key;
+    uint32_t sid_lo, sid_hi;
+    uint64_t block;
+    uint64_t buf1;
+    int pos;  // 0: buf empty, 1: buf1 holds the second half
+
+    __device__ __forceinline__ Stream(uint64_t seed, uint64_t sid)
+        : key(make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32))),
+          sid_lo(static_cast<uint32_t>(sid)), sid_hi(static_cast<uint32_t>(sid >> 32)),
+          block(0), buf1(0), pos(0) {}
+
+    __device__ __forceinline__ uint64_t next_u64() {
+        if (pos == 1) {
+            pos = 0;
+            return buf1;
+        }
+        const uint4 o = philox4x32_10(
+            make_uint4(static_cast<uint32_t>(block), static_cast<uint32_t>(block >> 32), sid_lo, sid_hi),
+            key);
+        ++block;
+        buf1 = (static_cast<uint64_t>(o.w) << 32) | o.z;
+        pos = 1;
+        return (static_cast<uint64_t>(o.y) << 32) | o.x;
+    }
+    // ((x >> 12) + 0.5) * 2^-52 (rng.hpp:41-43): exact in binary64.
+    __device__ __forceinline__ double next_uniform() {
+        return DMUL(DADD(static_cast<double>(next_u64() >> 12), 0.5), 0x1p-52);
+    }
+    // normal_quantile(next_uniform()) (rng.cpp:42-49)
+    __device__ __forceinline__ double next_normal() { return qrmc_normal_quantile(next_uniform()); }
+};
+
+__device__ __forceinline__ uint64_t sid_training(int step, uint64_t path) {
+    return (static_cast<uint64_t>(step) << kStepShift) | path;
+}
+__device__ __forceinline__ uint64_t sid_evaluation(int step, uint64_t point) {
+    return (uint64_t{1} << 63) | (static_cast<uint64_t>(step) << kStepShift) | point;
+}
+
+// ------------------------------------------------------------------ measure
+// Product Student-t measure for mu in {1, 2} (proj/src/student.cpp:53-106).
+
+
+// centered_cdf + center shift (student.cpp:53-63, 78-82)
+__device__ __forceinline__ double measure_cdf(const MeasureDev& m, double x, int l) {
+    x = DSUB(x, m.center[l]);
+    if (m.form == 1) return DADD(0.5, DDIV(atan(x), 3.14159265358979323846));
+    return DMUL(0.5, DADD(DDIV(x, __dsqrt_rn(DADD(DMUL(x, x), 1.0))), 1.0));
+}
+
+// inv_cdf with the 1e-15 guard band (student.cpp:65-76, 84-89)
+__device__ __forceinline__ double measure_inv_cdf(const MeasureDev& m, double u, int l) {
+    const double g = 1e-15;
+    u = u < g ? g : u;
+    u = (1.0 - g) < u ? (1.0 - g) : u;
+    double c;
+    if (m.form == 1)
+        c = tan(DMUL(3.14159265358979323846, DSUB(u, 0.5)));
+    else
+        c = DDIV(DSUB(u, 0.5), __dsqrt_rn(DMUL(u, DSUB(1.0, u))));
+    return DADD(c, m.center[l]);
+}
+
+// ------------------------------------------------------------------ problem
+// Device functors replacing ProblemSpec's std::function members
+// (sde.hpp:23-29; SinBenchmark functors benchmark.cpp:46-62).
+
+
+__device__ __forceinline__ double sum_of(const double* x, int d) {
+    double s = 0.0;
+    for (int l = 0; l < d; ++l) s = DADD(s, x[l]);
+    return s;
+}
+
+__device__ __forceinline__ double terminal(const ProblemDev& p, const double* x) {
+    switch (p.terminal_kind) {
+        case QRMC_TERMINAL_SIN_SUM: return DADD(DADD(1.0, p.tp0), sin(DMUL(p.tp1, sum_of(x, p.dim))));
+        case QRMC_TERMINAL_CONST: return p.tp0;
+        case QRMC_TERMINAL_X0: return x[0];
+        default: return DDIV(1.0, DSUB(x[0], x[0]));
+    }
+}
+
+__device__ __forceinline__ double driver(const ProblemDev& p, double t, const double* x, double y) {
+    switch (p.driver_kind) {
+        case QRMC_DRIVER_ZERO: return 0.0;
+        case QRMC_DRIVER_CONST: return p.dp0;
+        case QRMC_DRIVER_Y: return y;
+        default: {
+            // y - kappa - 1 - sin(lam sum x) * exp(lam*lam*d*(t-T)/2)  (benchmark.cpp:57-61)
+            const double e = exp(DDIV(DMUL(DMUL(DMUL(p.dp1, p.dp1), static_cast<double>(p.dim)),
+                                           DSUB(t, p.horizon)), 2.0));
+            const double z = DSUB(DSUB(DSUB(y, p.dp0), 1.0), DMUL(sin(DMUL(p.dp1, sum_of(x, p.dim))), e));
+            const double zz = DMUL(z, z);
+            return zz < 1.0 ? zz : 1.0;
+        }
+    }
+}
+
+// lstar_bound (sde.cpp:27-35)
+__device__ __forceinline__ double lstar(const ProblemDev& p, const double* x) {
+    if (p.eta == 0.0) return p.lstar_base;
+    double n2 = 0.0;
+    for (int l = 0; l < p.dim; ++l) n2 = DADD(n2, DMUL(x[l], x[l]));
+    return DMUL(p.lstar_base, pow(DADD(1.0, n2), DDIV(p.eta, 2.0)));
+}
+
+// damping_weight (solver.cpp:43-48)
+__device__ __forceinline__ double damping_weight(const double* x, int d, double q) {
+    if (q == 0.0) return 1.0;
+    double n2 = 0.0;
+    for (int l = 0; l < d; ++l) n2 = DADD(n2, DMUL(x[l], x[l]));
+    return pow(DADD(1.0, n2), DDIV(q, 2.0));
+}
+
+// truncate_soft (solver.cpp:37-41): std::min(std::max(v, -b), b)
+__device__ __forceinline__ double truncate_soft(double v, double b) {
+    const double lo = -b;
+    v = v < lo ? lo : v;
+    return b < v ? b : v;
+}
+
+// euler_step in place (sde.cpp:37-73). Returns 0 or the SimulationError step.
+__device__ __forceinline__ int euler_step(const ProblemDev& p, double* x, double sqrt_dt, double dt,
+                                          Stream& s, int j) {
+    double dw[kMaxDim];
+    for (int l = 0; l < p.bdim; ++l) dw[l] = DMUL(sqrt_dt, s.next_normal());
+    int bad = 0;
+    for (int l = 0; l < p.dim; ++l) {
+        const double out = p.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(p.sigma, dw[l]) : dw[l];
+        double v;
+        if (p.drift_kind == QRMC_DRIFT_CONST)
+            v = DADD(x[l], DADD(DMUL(p.drift_c, dt), out));
+        else
+            v = DADD(x[l], out);
+        x[l] = v;
+        if (!isfinite(v) || fabs(v) > p.state_bound) bad = j + 1;
+    }
+    return bad;
+}
+
+// ------------------------------------------------------------------ series
+// Student-cosine series  y(x) = sum_k alpha_k prod_l T_l[k_l]
+// (cosine_basis.cpp:67-112), evaluated by sum factorisation over Gamma's
+// lexicographic trie. The host packs alpha'_k = alpha_k * sqrt2^{nnz(k)} so
+// the device works with plain Chebyshev values c_l[v] = cos(v * pi * u_l)
+// (T_l[v] = sqrt2 c_l[v] for v >= 1, T_l[0] = c_l[0] = 1). The node program
+// holds one word per leaf run: bits 0..3 = level L whose index advanced
+// from the previous run (deeper levels reset to 0; lexicographic order of a
+// downward-closed set guarantees exactly this transition), bits 4.. = run
+// length R (leaf indices 0..R-1). Runs are padded to even length in alpha'.
+//
+// Horner over the trie: acc[l] accumulates sum_v c_l[v] V(prefix + v) for
+// the current prefix of length l; a finished run folds into acc[D-2], a
+// finished level-l node folds into acc[l-1].
+template <int D>
+__device__ __forceinline__ double series_eval(const double* __restrict__ alpha,
+                                              const uint32_t* __restrict__ prog, int n_runs,
+                                              const double (&c1)[D]) {
+    double two_c1[D], cur[D], prev[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        two_c1[l] = 2.0 * c1[l];
+        cur[l] = 1.0;
+        prev[l] = c1[l];  // c_{-1} = c_1: the recurrence then yields c_1 = 2 c1 * 1 - c1 = c1 exactly
+    }
+    constexpr int NA = D > 1 ? D - 1 : 1;
+    double acc[NA];
+#pragma unroll
+    for (int l = 0; l < NA; ++l) acc[l] = 0.0;
+    double y = 0.0;
+    const double2* a2 = reinterpret_cast<const double2*>(alpha);
+    for (int n = 0; n < n_runs; ++n) {
+        const uint32_t w = __ldg(prog + n);
+        const int L = static_cast<int>(w & 15u);
+        const int R = static_cast<int>(w >> 4);
+        if constexpr (D >= 2) {
+            if (n > 0) {
+                // close levels L+1..D-2 (fold into the parent), then advance level L
+#pragma unroll
+                for (int l = D - 3; l >= 0; --l) {
+                    if (l >= L) {
+                        acc[l] = fma(cur[l], acc[l + 1], acc[l]);
+                        acc[l + 1] = 0.0;
+                    }
+                }
+#pragma unroll
+                for (int l = 0; l < D - 1; ++l) {
+                    if (l == L) {
+                        const double nx = fma(two_c1[l], cur[l], -prev[l]);
+                        prev[l] = cur[l];
+                        cur[l] = nx;
+                    } else if (l > L) {
+                        cur[l] = 1.0;
+                        prev[l] = c1[l];
+                    }
+                }
+            }
+        }
+        // leaf run: s = sum_{b<R} alpha'[b] c_{D-1}[b]
+        double s0 = 0.0, s1 = 0.0;
+        double cp = c1[D - 1], cc = 1.0;
+        const double tc = two_c1[D - 1];
+        const int pairs = (R + 1) >> 1;
+        for (int b = 0; b < pairs; ++b) {
+            const double2 a = __ldg(a2 + b);
+            const double cn = fma(tc, cc, -cp);
+            s0 = fma(a.x, cc, s0);
+            s1 = fma(a.y, cn, s1);
+            const double c2 = fma(tc, cn, -cc);
+            cp = cn;  // (cp, cc) = (c_{2b+1}, c_{2b+2})
+            cc = c2;
+        }
+        a2 += pairs;
+        const double s = s0 + s1;
+        if constexpr (D >= 2)
+            acc[D - 2] = fma(cur[D - 2], s, acc[D - 2]);
+        else
+            y += s;
+    }
+    if constexpr (D >= 2) {
+#pragma unroll
+        for (int l = D - 3; l >= 0; --l) acc[l] = fma(cur[l], acc[l + 1], acc[l]);
+        y = acc[0];
+    }
+    return y;
+}
+
+}  // namespace qrmc_dev

@@ -1,0 +1,31 @@
+// qrmc_types.h -- plain structs shared by host.cpp and the kernels (no device code).
+#pragma once
+
+#include <cstdint>
+
+namespace qrmc_dev {
+
+constexpr int kLanes = 256;  // LaneLayout::kLanes (proj/include/qrmc/parallel.hpp:22)
+constexpr int kChunk = 1024; // LaneLayout::kChunk (parallel.hpp:21)
+constexpr unsigned kStepShift = 40;  // stream_ids::kStepShift (rng.hpp:77)
+constexpr int kMaxDim = 8;
+
+// Product Student-t measure for mu in {1, 2} (proj/src/student.cpp:53-106).
+struct MeasureDev {
+    int form;  // 1 Cauchy, 2 algebraic mu=2
+    double center[kMaxDim];
+};
+
+// Device functors replacing ProblemSpec's std::function members
+// (sde.hpp:23-29; SinBenchmark functors benchmark.cpp:46-62).
+struct ProblemDev {
+    int dim, bdim;
+    double horizon;
+    int terminal_kind, driver_kind, drift_kind, diffusion_kind;
+    double tp0, tp1, dp0, dp1, drift_c, sigma;
+    double lstar_base;  // C_eta (C_g + T C_f) exp(C_eta L_f T), host-computed exactly as sde.cpp:28-29
+    double eta;         // max(eta_g, eta_f)
+    double state_bound;
+};
+
+}  // namespace qrmc_dev
