@@ -1,0 +1,343 @@
+#!/usr/bin/env python3
+"""Benchmark: full GQRMDP backward solve on B200 (path-steps/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" of this benchmark is one full backward solve (qrmc::backward_solve,
+proj/src/solver.cpp:109-226) of the BASELINE.json configs[1] workload as
+restated in SURVEY.md 8(d): SinBenchmark d=4 (kappa 0.6, lambda 1/2, T=1),
+hyperbolic index set Gamma_H(4,100) (#Gamma = 12,752), damping q = 5.1,
+N = 20 time steps, M = 2e7 paths per GPU per backward step (weak scaling),
+Student mu=2 sampling measure, training seed 42, store-cloud mode.
+
+Metric: simulated path-steps per second = M N (N+1)/2 / solve time
+(SURVEY.md 8(d)); `value` is device-timed (CUDA events on the solver's
+stream, inputs resident), `e2e` goes through the public C ABI call
+qrmc_gpu_backward_solve with host buffers. With --impl reference the same
+metric is measured for the reference's own CPU solver (oracle/_ref, the
+unmodified reference sources) on a bounded sample of M on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+WORKLOAD = dict(name="sinbench-d4-hyperbolic100-q5.1-N20", dim=4, kappa=0.6, lam=0.0, horizon=1.0,
+                gamma_kind="hyperbolic", degrees=(100,), damping=5.1, steps=20, mu=2.0, seed=42)
+DEFAULT_PATHS_PER_GPU = 20_000_000
+CPU_SAMPLE_PATHS = 16_384  # 16 lanes of 1024 paths: saturates 16 host cores (parallel.hpp:21-22)
+METRIC = "simulated paths x time-steps per second per full backward solve"
+UNIT = "path-steps/s"
+
+
+def peaks() -> dict:
+    p = {}
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        p.update(json.loads(f.read_text()))
+    # FP64 peak measured on this pool's B200 (profiles/r01_fp64_peak.txt: DMMA m8n8k4
+    # 37.1 TF/s, DFMA 34.2 TF/s, cuBLAS DGEMM 35.5 TF/s). MEASURED_PEAKS.json has no FP64 entry.
+    p.setdefault("fp64_tflops", 37.1)
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def path_steps(m: int, n: int) -> int:
+    return m * n * (n + 1) // 2
+
+
+def flops_alg(k: int, m: int, n: int) -> float:
+    # 2 FLOPs (one FMA) per basis term per path-step
+    return float(k) * m * n * (n + 1)
+
+
+def make_problem_config(paths: int):
+    from paper_2407_21084_b200 import _abi
+    w = WORKLOAD
+    prob = _abi.sin_bench_problem(w["dim"], w["kappa"], w["lam"], w["horizon"])
+    cfg = _abi.ConfigHolder(steps=w["steps"], paths=paths, damping=w["damping"], seed=w["seed"],
+                            gamma_kind=_abi.GAMMA_KINDS[w["gamma_kind"]], degrees=w["degrees"], mu=w["mu"])
+    return prob, cfg
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ reference CPU
+def cpu_reference_solve(paths: int) -> tuple[float, int]:
+    """Wall time of the reference's own backward_solve (oracle/_ref) on all host cores."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles  # test infrastructure: the reference build, only for the baseline leg
+    from paper_2407_21084_b200 import _abi
+    R = oracles.ref() if oracles.have_ref() else None
+    kind = "reference"
+    if R is None:
+        R = oracles.port()
+        kind = "port"
+    prob, cfg = make_problem_config(paths)
+    k = int(_abi.lib().qrmc_gpu_gamma_size(cfg.c.gamma_kind, prob.dim, cfg.c.degrees, cfg.c.n_degrees)) \
+        if _abi.LIB_PATH.exists() else 12752
+    t0 = time.perf_counter()
+    R.backward_solve(prob, cfg, k)
+    return time.perf_counter() - t0, kind
+
+
+def run_reference_arm(args) -> int:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    n = WORKLOAD["steps"]
+    paths = args.cpu_paths
+    cores = os.cpu_count() or 1
+    threads = min(cores, 256, -(-paths // 1024))
+    for _ in range(args.warmup):
+        cpu_reference_solve(paths)
+    times = []
+    kind = "reference"
+    for _ in range(args.steps):
+        t, kind = cpu_reference_solve(paths)
+        times.append(t)
+    mean = sum(times) / len(times)
+    value = path_steps(paths, n) / mean
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD["name"], "paths_per_step_sample": paths, "N": n,
+                   "basis": "hyperbolic(4,100) #Gamma=12752", "parallelism": "host threads (lane pool)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"full N={n} backward solve at M={paths} (work is exactly linear in M)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args) -> int:
+    from paper_2407_21084_b200 import _abi, api
+    world, rank, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    L = _abi.lib()
+    err = C.create_string_buffer(1024)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            api.raise_for(L.qrmc_gpu_nccl_unique_id(uid, err, 1024), err.value.decode())
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        C.memmove(uid, obj[0], 128)
+        uid_ptr = C.cast(uid, C.c_void_p)
+    else:
+        uid_ptr = None
+    session = C.c_void_p()
+    api.raise_for(L.qrmc_gpu_session_create(local, rank, world, uid_ptr, C.byref(session), err, 1024),
+                  err.value.decode())
+
+    paths_total = args.paths * world  # weak scaling: M per GPU fixed
+    n = WORKLOAD["steps"]
+    prob, cfg = make_problem_config(paths_total)
+    plan = C.c_void_p()
+    api.raise_for(L.qrmc_gpu_plan_create(session, C.byref(prob), cfg.ref(), C.byref(plan), err, 1024),
+                  err.value.decode())
+    K = int(L.qrmc_gpu_plan_basis_size(plan))
+    stream = torch.cuda.ExternalStream(L.qrmc_gpu_plan_stream(plan))
+    stats = _abi.Stats()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def run_once():
+        api.raise_for(L.qrmc_gpu_plan_run(plan, C.byref(stats), err, 1024), err.value.decode(), stats.error_step)
+
+    for _ in range(args.warmup):
+        run_once()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kernel_s = np.zeros(3)
+    ks = (C.c_double * 3)()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            run_once()
+            api.raise_for(L.qrmc_gpu_plan_kernel_seconds(plan, ks, None, err, 1024), err.value.decode())
+            kernel_s += np.array(ks[:])
+        ev1.record(stream)
+        barrier()
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    if dist is not None:
+        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    per_solve = elapsed / args.steps
+    value = path_steps(paths_total, n) / per_solve
+    launches = int(stats.kernel_launches) * args.steps
+
+    # roofline of the dominant kernel, k_responses (phase 1): 2 FLOPs per basis term per
+    # future-point evaluation, M_local * sum_i (N-1-i) evaluations per solve.
+    m_local = args.paths
+    resp_flops = 2.0 * K * m_local * n * (n - 1) / 2.0
+    resp_s = kernel_s[0] / args.steps
+    pk = peaks()
+    achieved = resp_flops / resp_s / 1e12
+    solve_tflops = flops_alg(K, m_local, n) / per_solve / 1e12
+
+    # e2e: the public C ABI call with host buffers (plan build + H2D, graph, solve, D2H)
+    h2d, d2h = C.c_uint64(), C.c_uint64()
+    L.qrmc_gpu_plan_io_bytes(plan, C.byref(h2d), C.byref(d2h))
+    coeffs = np.zeros((n, K))
+    e2e_times = []
+    for _ in range(args.e2e_steps):
+        barrier()
+        t0 = time.perf_counter()
+        st = L.qrmc_gpu_backward_solve(session, C.byref(prob), cfg.ref(),
+                                       coeffs.ctypes.data_as(C.POINTER(C.c_double)), coeffs.size, None,
+                                       C.byref(stats), err, 1024)
+        api.raise_for(st, err.value.decode(), stats.error_step)
+        barrier()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_t = sum(e2e_times) / len(e2e_times)
+    if dist is not None:
+        t = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    L.qrmc_gpu_plan_destroy(plan)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_cpu, kind = cpu_reference_solve(args.cpu_paths)
+        cores = os.cpu_count() or 1
+        cpu = {"value": path_steps(args.cpu_paths, n) / t_cpu, "unit": UNIT,
+               "cores": min(cores, 256, -(-args.cpu_paths // 1024)), "kind": kind,
+               "sample": f"one full N={n} backward solve at M={args.cpu_paths} (work exactly linear in M), "
+                         f"{t_cpu:.1f} s on the box's host cores"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_solve * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD["name"], "d": WORKLOAD["dim"], "basis": "hyperbolic(4,100)",
+                       "basis_size": K, "N": n, "paths_per_gpu": args.paths, "paths_total": paths_total,
+                       "damping": WORKLOAD["damping"], "seed": WORKLOAD["seed"],
+                       "parallelism": f"paths sharded by lane over {world} GPU(s)",
+                       "l2": "working set (cloud + responses, 0.8 GB/GPU) larger than L2"},
+            "time_to_solution_s": per_solve,
+            "fp64_solve_tflops": solve_tflops,
+            "fp64_solve_frac": solve_tflops / pk["fp64_tflops"],
+            "kernel_seconds_per_solve": {"k_responses": kernel_s[0] / args.steps,
+                                         "k_project": kernel_s[1] / args.steps,
+                                         "k_finish_step": kernel_s[2] / args.steps},
+            "roofline": {"kernel": "k_responses", "bound": "fp64", "achieved": achieved,
+                         "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"],
+                         "traffic": None,
+                         "peak_source": "measured FP64 (DMMA 37.1 TF/s) on this pool, profiles/r01_fp64_peak.txt"},
+            "e2e": {"value": path_steps(paths_total, n) / e2e_t, "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value)},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    L.qrmc_gpu_session_destroy(session)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--paths", type=int, default=DEFAULT_PATHS_PER_GPU, help="paths per GPU per backward step")
+    ap.add_argument("--cpu-paths", type=int, default=CPU_SAMPLE_PATHS)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

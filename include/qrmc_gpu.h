@@ -168,6 +168,20 @@ qrmc_status qrmc_gpu_plan_run(qrmc_gpu_plan_t* plan, qrmc_stats_t* stats, char* 
 qrmc_status qrmc_gpu_plan_download(qrmc_gpu_plan_t* plan, double* coeffs, size_t coeffs_len,
                                    char* err, size_t err_len);
 int64_t qrmc_gpu_plan_basis_size(const qrmc_gpu_plan_t* plan);
+/* Device seconds of the last run per kernel kind, summed over steps:
+ * out3 = {k_responses, k_project (+ the NCCL exchange), k_finish_step};
+ * per_step (steps x 3, row i = cloud step i) or NULL. CUDA-event timed inside the graph. */
+qrmc_status qrmc_gpu_plan_kernel_seconds(const qrmc_gpu_plan_t* plan, double* out3, double* per_step,
+                                         char* err, size_t err_len);
+/* Multi-GPU path sharding (host-only, no device needed): rank `rank` of `world`
+ * owns the reference's lanes [lane_lo, lane_hi) (LaneLayout, parallel.hpp:20-36:
+ * chunk c of 1024 paths belongs to lane c % 256) and n_owned paths. */
+qrmc_status qrmc_gpu_lane_ownership(int64_t paths, int32_t rank, int32_t world, int32_t* lane_lo,
+                                    int32_t* lane_hi, int64_t* n_owned);
+/* The kernels' owned index -> global path id map, exported for host-side tests. */
+int64_t qrmc_gpu_owned_path(int64_t q, int32_t lane_lo, int32_t owned_lanes);
+/* Host->device and device->host bytes one qrmc_gpu_backward_solve call moves. */
+qrmc_status qrmc_gpu_plan_io_bytes(const qrmc_gpu_plan_t* plan, uint64_t* h2d, uint64_t* d2h);
 /* The CUDA stream every kernel of the plan is launched on (cudaStream_t). */
 void* qrmc_gpu_plan_stream(const qrmc_gpu_plan_t* plan);
 void qrmc_gpu_plan_destroy(qrmc_gpu_plan_t* plan);

@@ -396,12 +396,16 @@ struct qrmc_gpu_plan {
     DevBuf<unsigned long long> d_counters;
     DevBuf<int> d_flags;
     cudaGraphExec_t graph = nullptr;
-    std::vector<cudaEvent_t> step_events;  // N+1 events bracketing the steps
+    // 3N+1 events: ev[0] before the first kernel, then one after each kernel;
+    // step i's kernels (responses, project[+exchange], finish) end at
+    // ev[3(N-1-i)+1 .. 3(N-1-i)+3].
+    std::vector<cudaEvent_t> ev;
     int launches_per_run = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;
 
     ~qrmc_gpu_plan() {
         if (graph) cudaGraphExecDestroy(graph);
-        for (auto e : step_events) cudaEventDestroy(e);
+        for (auto e : ev) cudaEventDestroy(e);
     }
 };
 
@@ -445,12 +449,17 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
     cuda_check(cudaMemsetAsync(P.d_flags.p, 0, sizeof(int), st), "memset");
     // flags[1] = 0x7f7f7f7f: "no SimulationError step yet" for atomicMin
     cuda_check(cudaMemsetAsync(P.d_flags.p + 1, 0x7f, sizeof(int), st), "memset");
-    if (with_events) cuda_check(cudaEventRecordWithFlags(P.step_events[0], st, cudaEventRecordExternal), "event");
+    int e = 0;
+    auto mark = [&] {
+        if (with_events) cuda_check(cudaEventRecordWithFlags(P.ev[e++], st, cudaEventRecordExternal), "event");
+    };
+    mark();
     const int world = P.session->world;
     for (int i = N - 1; i >= 0; --i) {
         StepArgs a = P.base;
         a.step = i;
         cuda_check(launch_responses(a, st), "k_responses");
+        mark();
         ProjArgs pa = P.proj;
         pa.partials = P.d_partials.p + static_cast<size_t>(P.session->rank) * P.lanes_per_rank * P.K;
         cuda_check(launch_project(a, pa, st), "k_project");
@@ -459,6 +468,7 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
                                         ncclDouble, P.session->comm, st),
                        "ncclAllGather");
         }
+        mark();
         FinishArgs f{};
         f.all_partials = P.d_partials.p;
         f.basis_size = P.K;
@@ -467,7 +477,7 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
         f.pack_pos = P.d_pack_pos.p;
         f.pack_scale = P.d_pack_scale.p;
         cuda_check(launch_finish(a, f, st), "k_finish_step");
-        if (with_events) cuda_check(cudaEventRecordWithFlags(P.step_events[N - i], st, cudaEventRecordExternal), "event");
+        mark();
     }
 }
 
@@ -489,7 +499,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
 
     // lane ownership: rank g owns lanes [g*lpr, min(256, (g+1)*lpr))
     P->lanes_per_rank = (kLanes + s->world - 1) / s->world;
-    const int lo = s->rank * P->lanes_per_rank;
+    const int lo = std::min(kLanes, s->rank * P->lanes_per_rank);
     const int hi = std::min(kLanes, lo + P->lanes_per_rank);
     const int64_t chunks = (cfg.paths + kChunk - 1) / kChunk;
     int64_t n_owned = 0;
@@ -558,9 +568,13 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     pa.basis_size = P->K;
 
     cuda_check(configure_project(d, project_smem_bytes(pa)), "k_project attributes");
-    P->step_events.resize(static_cast<size_t>(cfg.steps) + 1);
-    for (auto& e : P->step_events) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    P->ev.resize(3 * static_cast<size_t>(cfg.steps) + 1);
+    for (auto& e : P->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     P->launches_per_run = 3 * cfg.steps;
+    P->h2d_bytes = pg.prog.size() * sizeof(uint32_t) + P->gamma.rows.size() * sizeof(int32_t) +
+                   pg.pack_pos.size() * sizeof(int32_t) + pg.pack_scale.size() * sizeof(double);
+    P->d2h_bytes = static_cast<uint64_t>(cfg.steps) * P->K * sizeof(double) + 2 * sizeof(unsigned long long) +
+                   2 * sizeof(int);
 
     if (s->world == 1) {
         cudaGraph_t g;
@@ -592,12 +606,12 @@ void run_plan(qrmc_gpu_plan& P, qrmc_stats_t* stats, double* step_wall) {
     cuda_check(cudaMemcpy(counters, P.d_counters.p, sizeof counters, cudaMemcpyDeviceToHost), "D2H");
     cuda_check(cudaMemcpy(flags, P.d_flags.p, sizeof flags, cudaMemcpyDeviceToHost), "D2H");
     float ms = 0.f;
-    cuda_check(cudaEventElapsedTime(&ms, P.step_events[0], P.step_events[P.steps]), "event time");
+    cuda_check(cudaEventElapsedTime(&ms, P.ev.front(), P.ev.back()), "event time");
     if (step_wall) {
         for (int i = 0; i < P.steps; ++i) {
+            const int b = 3 * (P.steps - 1 - i);
             float t = 0.f;
-            cuda_check(cudaEventElapsedTime(&t, P.step_events[P.steps - 1 - i], P.step_events[P.steps - i]),
-                       "event time");
+            cuda_check(cudaEventElapsedTime(&t, P.ev[b], P.ev[b + 3]), "event time");
             step_wall[i] = t * 1e-3;
         }
     }
@@ -743,6 +757,56 @@ qrmc_status qrmc_gpu_plan_download(qrmc_gpu_plan_t* plan, double* coeffs, size_t
 
 int64_t qrmc_gpu_plan_basis_size(const qrmc_gpu_plan_t* plan) { return plan ? plan->K : -1; }
 
+qrmc_status qrmc_gpu_plan_kernel_seconds(const qrmc_gpu_plan_t* plan, double* out3, double* per_step,
+                                         char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!plan || !out3) fail(QRMC_EINVAL, "plan_kernel_seconds: null argument");
+        const int N = plan->steps;
+        out3[0] = out3[1] = out3[2] = 0.0;
+        for (int s = 0; s < N; ++s) {
+            for (int k = 0; k < 3; ++k) {
+                float t = 0.f;
+                cuda_check(cudaEventElapsedTime(&t, plan->ev[3 * s + k], plan->ev[3 * s + k + 1]), "event time");
+                out3[k] += t * 1e-3;
+                // per_step rows are indexed by the cloud step i = N-1-s
+                if (per_step) per_step[3 * (N - 1 - s) + k] = t * 1e-3;
+            }
+        }
+    });
+}
+
+qrmc_status qrmc_gpu_lane_ownership(int64_t paths, int32_t rank, int32_t world, int32_t* lane_lo,
+                                    int32_t* lane_hi, int64_t* n_owned) {
+    if (paths < 1 || world < 1 || rank < 0 || rank >= world || !lane_lo || !lane_hi || !n_owned)
+        return QRMC_EINVAL;
+    const int lpr = (kLanes + world - 1) / world;
+    const int lo = std::min(kLanes, rank * lpr);
+    const int hi = std::min(kLanes, lo + lpr);
+    const int64_t chunks = (paths + kChunk - 1) / kChunk;
+    int64_t n = 0;
+    for (int lane = lo; lane < hi; ++lane)
+        for (int64_t c = lane; c < chunks; c += kLanes) n += std::min<int64_t>(kChunk, paths - c * kChunk);
+    *lane_lo = lo;
+    *lane_hi = hi;
+    *n_owned = n;
+    return QRMC_OK;
+}
+
+int64_t qrmc_gpu_owned_path(int64_t q, int32_t lane_lo, int32_t owned_lanes) {
+    // the device's owned-index -> path map (kernels.cu owned_to_path), exported for host tests
+    const int64_t cq = q / kChunk;
+    const int64_t r = cq / owned_lanes;
+    const int64_t lane = lane_lo + cq % owned_lanes;
+    return (r * kLanes + lane) * kChunk + q % kChunk;
+}
+
+qrmc_status qrmc_gpu_plan_io_bytes(const qrmc_gpu_plan_t* plan, uint64_t* h2d, uint64_t* d2h) {
+    if (!plan || !h2d || !d2h) return QRMC_EINVAL;
+    *h2d = plan->h2d_bytes;
+    *d2h = plan->d2h_bytes;
+    return QRMC_OK;
+}
+
 void* qrmc_gpu_plan_stream(const qrmc_gpu_plan_t* plan) {
     return plan ? static_cast<void*>(plan->session->stream) : nullptr;
 }
@@ -765,15 +829,19 @@ qrmc_status qrmc_gpu_backward_solve(qrmc_gpu_session_t* session, const qrmc_prob
     }
     return guarded(err, err_len, [&] {
         if (!problem || !config) fail(QRMC_EINVAL, "backward_solve: null argument");
+        // validate everything host-side before touching a device, in the
+        // reference's order: spec.validate(), config.validate(spec) (solver.cpp:110-111)
+        to_device_problem(*problem);
+        validate_config(*config);
+        const Gamma g = build_gamma(config->gamma_kind, problem->dim, config->degrees, config->n_degrees);
+        to_device_measure(*config, problem->dim);
+        if (!coeffs || coeffs_len < static_cast<size_t>(g.size()) * static_cast<size_t>(config->steps))
+            fail(QRMC_EINVAL, "coefficient buffer too small");
         std::unique_ptr<qrmc_gpu_session, void (*)(qrmc_gpu_session*)> own(nullptr, destroy_session);
         if (!session) {
             own.reset(make_session(current_device(), 0, 1, nullptr).release());
             session = own.get();
         }
-        // validate the output buffer before any device work
-        const Gamma g = build_gamma(config->gamma_kind, problem->dim, config->degrees, config->n_degrees);
-        if (!coeffs || coeffs_len < static_cast<size_t>(g.size()) * static_cast<size_t>(std::max(config->steps, 0)))
-            fail(QRMC_EINVAL, "coefficient buffer too small");
         auto P = make_plan(session, *problem, *config);
         run_plan(*P, stats, step_wall_seconds);
         download(*P, coeffs, coeffs_len);
