@@ -183,7 +183,39 @@ struct Program {
     std::vector<int32_t> pack_pos;
     std::vector<double> pack_scale;
     int64_t kp = 0;
+    // shared-memory tiles of the program (series_block.cuh)
+    std::vector<int4> tiles;
+    std::vector<uint32_t> tile_prog;
 };
+
+constexpr int kHostTileA = 2048;  // == kTileA in series_block.cuh
+constexpr int kHostTileP = 1024;  // == kTileP
+constexpr uint32_t kFirstRunCode = 15;
+
+void build_tiles(Program& p) {
+    int4 cur = make_int4(0, 0, 0, 0);
+    int64_t alpha_pos = 0;
+    auto close = [&] {
+        if (cur.y == 0) return;
+        p.tiles.push_back(cur);
+        while (p.tile_prog.size() % 4) p.tile_prog.push_back(0);
+    };
+    for (uint32_t w : p.prog) {
+        const int64_t R = w >> 4;
+        const int64_t padded = (R + 1) & ~int64_t{1};
+        if (padded > kHostTileA) fail(QRMC_ENOTIMPL, fmt("leaf run of %lld coefficients exceeds a tile", (long long)R));
+        if (cur.y == kHostTileP || cur.w + padded > kHostTileA) {
+            close();
+            cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0);
+        }
+        if (cur.y == 0) cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0);
+        p.tile_prog.push_back(w);
+        cur.y += 1;
+        cur.w += static_cast<int>(padded);
+        alpha_pos += padded;
+    }
+    close();
+}
 
 Program build_program(const Gamma& g) {
     Program p;
@@ -208,8 +240,9 @@ Program build_program(const Gamma& g) {
             ++j;
         }
         const int64_t R = j - i;
-        int L = 0;
-        if (!prev_prefix.empty()) {
+        int L = static_cast<int>(kFirstRunCode);
+        if (i > 0) {
+            L = 0;
             while (L < d - 1 && prev_prefix[L] == row[L]) ++L;
             if (L >= d - 1 || row[L] != prev_prefix[L] + 1)
                 fail(QRMC_ELOGIC, "index set is not downward closed (node transition)");
@@ -232,6 +265,7 @@ Program build_program(const Gamma& g) {
         i = j;
     }
     p.kp = std::max<int64_t>(pos, 2);
+    build_tiles(p);
     return p;
 }
 
@@ -390,7 +424,8 @@ struct qrmc_gpu_plan {
     int64_t K = 0;
     int steps = 0;
     int lanes_per_rank = kLanes;
-    DevBuf<uint32_t> d_prog;
+    DevBuf<uint32_t> d_prog, d_tile_prog;
+    DevBuf<int4> d_tiles;
     DevBuf<int32_t> d_rows, d_pack_pos;
     DevBuf<double> d_pack_scale, d_alpha, d_coef, d_partials, d_resp, d_cloud;
     DevBuf<unsigned long long> d_counters;
@@ -458,7 +493,8 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
     for (int i = N - 1; i >= 0; --i) {
         StepArgs a = P.base;
         a.step = i;
-        cuda_check(launch_responses(a, st), "k_responses");
+        SeriesTiles t{P.d_tiles.p, static_cast<int>(P.d_tiles.n), P.d_tile_prog.p};
+        cuda_check(launch_responses(a, t, st), "k_responses");
         mark();
         ProjArgs pa = P.proj;
         pa.partials = P.d_partials.p + static_cast<size_t>(P.session->rank) * P.lanes_per_rank * P.K;
@@ -511,6 +547,10 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     const Program& pg = P->program;
     P->d_prog.alloc(pg.prog.size());
     P->d_prog.upload(pg.prog.data(), pg.prog.size(), st);
+    P->d_tiles.alloc(pg.tiles.size());
+    P->d_tiles.upload(pg.tiles.data(), pg.tiles.size(), st);
+    P->d_tile_prog.alloc(pg.tile_prog.size());
+    P->d_tile_prog.upload(pg.tile_prog.data(), pg.tile_prog.size(), st);
     P->d_rows.alloc(P->gamma.rows.size());
     P->d_rows.upload(P->gamma.rows.data(), P->gamma.rows.size(), st);
     P->d_pack_pos.alloc(pg.pack_pos.size());
@@ -572,7 +612,8 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     for (auto& e : P->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     P->launches_per_run = 3 * cfg.steps;
     P->h2d_bytes = pg.prog.size() * sizeof(uint32_t) + P->gamma.rows.size() * sizeof(int32_t) +
-                   pg.pack_pos.size() * sizeof(int32_t) + pg.pack_scale.size() * sizeof(double);
+                   pg.pack_pos.size() * sizeof(int32_t) + pg.pack_scale.size() * sizeof(double) +
+                   pg.tiles.size() * sizeof(int4) + pg.tile_prog.size() * sizeof(uint32_t);
     P->d2h_bytes = static_cast<uint64_t>(cfg.steps) * P->K * sizeof(double) + 2 * sizeof(unsigned long long) +
                    2 * sizeof(int);
 

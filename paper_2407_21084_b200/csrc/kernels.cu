@@ -16,6 +16,7 @@
 
 #include "kernels.cuh"
 #include "qrmc_device.cuh"
+#include "series_block.cuh"
 
 namespace qrmc_dev {
 
@@ -49,52 +50,99 @@ __device__ __forceinline__ double eval_at(const StepArgs& a, const double* alpha
 }
 
 // ---------------------------------------------------------------- K1
+// P paths per thread, 128 threads per CTA; the CTA walks the backward step's
+// future time points in lockstep so that each coefficient row alpha_{j+1}
+// streams through shared memory once per CTA (series_block.cuh).
 template <int D>
-__global__ void __launch_bounds__(128) k_responses(const StepArgs a) {
-    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+struct K1Shape;
+template <> struct K1Shape<1> { static constexpr int P = 4, LT = 16; };
+template <> struct K1Shape<2> { static constexpr int P = 2, LT = 32; };
+template <> struct K1Shape<3> { static constexpr int P = 2, LT = 16; };
+template <> struct K1Shape<4> { static constexpr int P = 2, LT = 8; };
+template <> struct K1Shape<5> { static constexpr int P = 2, LT = 8; };
+template <> struct K1Shape<6> { static constexpr int P = 2, LT = 8; };
+template <> struct K1Shape<7> { static constexpr int P = 1, LT = 8; };
+template <> struct K1Shape<8> { static constexpr int P = 1, LT = 8; };
+
+constexpr int kK1Threads = 128;
+
+template <int D>
+__global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a, const SeriesTiles st) {
+    constexpr int P = K1Shape<D>::P, LT = K1Shape<D>::LT;
+    __shared__ SeriesSmem sm;
+    __shared__ int s_abort;
+    if (threadIdx.x == 0) s_abort = *a.abort_flag;
+    __syncthreads();
+    if (s_abort) return;  // uniform per CTA
+
+    int64_t q[P];
+    bool valid[P];
+    double xj[P][D], xn[P][D], w0[P], dsum[P];
+    int bad[P];
     uint32_t apps = 0, clipped = 0;
-    if (q < a.n_owned && !*a.abort_flag) {
-        const int64_t m = owned_to_path(a, q);
-        Stream s(a.seed, sid_training(a.step, static_cast<uint64_t>(m)));
-        double x0[D], xj[D], xn[D];
-        sample_start(a.meas, D, s, x0);
+    Stream st_p[P];
 #pragma unroll
-        for (int l = 0; l < D; ++l) xj[l] = x0[l];
-        double driver_sum = 0.0;
-        int bad = 0;
-        for (int j = a.step; j < a.steps; ++j) {
+    for (int p = 0; p < P; ++p) {
+        q[p] = (static_cast<int64_t>(blockIdx.x) * P + p) * kK1Threads + threadIdx.x;
+        valid[p] = q[p] < a.n_owned;
+        const int64_t qq = valid[p] ? q[p] : 0;
+        const int64_t m = owned_to_path(a, qq);
+        st_p[p] = Stream(a.seed, sid_training(a.step, static_cast<uint64_t>(m)));
 #pragma unroll
-            for (int l = 0; l < D; ++l) xn[l] = xj[l];
-            const int b = euler_step(a.prob, xn, a.sqrt_dt, a.dt, s, j);
-            if (b) {
-                bad = b;
-                break;
-            }
-            double y_next;
-            if (j + 1 == a.steps) {
-                y_next = terminal(a.prob, xn);  // exact initialisation (solver.cpp:69-72)
-            } else {
-                const double* row = a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp;
-                y_next = DMUL(eval_at<D>(a, row, xn), damping_weight(xn, D, a.q));
-            }
-            const double c = truncate_soft(y_next, lstar(a.prob, xn));
-            ++apps;
-            if (c != y_next) ++clipped;
-            driver_sum = DADD(driver_sum, driver(a.prob, DMUL(static_cast<double>(j), a.dt), xj, c));
+        for (int l = 0; l < D; ++l) xj[p][l] = measure_inv_cdf(a.meas, st_p[p].next_uniform(), l);
+        w0[p] = damping_weight<D>(xj[p], a.q);
+        if (a.cloud && valid[p]) {
 #pragma unroll
-            for (int l = 0; l < D; ++l) xj[l] = xn[l];
+            for (int l = 0; l < D; ++l) a.cloud[l * a.n_owned + q[p]] = xj[p][l];
         }
-        if (bad) {
-            record_error(a.err_flags, QRMC_ESIM, bad);
-        } else {
-            const double term = terminal(a.prob, xj);
-            const double v = DDIV(DADD(term, DMUL(a.dt, driver_sum)), damping_weight(x0, D, a.q));
-            if (!isfinite(v)) record_error(a.err_flags, QRMC_ENUMERIC, 0);
-            a.resp[q] = v;
-            if (a.cloud) {
+        dsum[p] = 0.0;
+        bad[p] = 0;
+    }
+    for (int j = a.step; j < a.steps; ++j) {
+        double y[P];
 #pragma unroll
-                for (int l = 0; l < D; ++l) a.cloud[l * a.n_owned + q] = x0[l];
+        for (int p = 0; p < P; ++p) {
+#pragma unroll
+            for (int l = 0; l < D; ++l) xn[p][l] = xj[p][l];
+            const int b = euler_step<D>(a.prob, xn[p], a.sqrt_dt, a.dt, st_p[p], j);
+            if (b && !bad[p]) bad[p] = b;
+        }
+        if (j + 1 == a.steps) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) y[p] = terminal<D>(a.prob, xn[p]);  // exact initialisation (solver.cpp:69-72)
+        } else {
+            double c1[P][D], ys[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+#pragma unroll
+                for (int l = 0; l < D; ++l)
+                    c1[p][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xn[p][l], l)));
+            series_block<D, P, LT>(sm, st, a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp, c1, ys);
+#pragma unroll
+            for (int p = 0; p < P; ++p) y[p] = DMUL(ys[p], damping_weight<D>(xn[p], a.q));
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const double c = truncate_soft(y[p], lstar<D>(a.prob, xn[p]));
+            if (valid[p]) {
+                ++apps;
+                if (c != y[p]) ++clipped;
             }
+            dsum[p] = DADD(dsum[p], driver<D>(a.prob, DMUL(static_cast<double>(j), a.dt), xj[p], c));
+#pragma unroll
+            for (int l = 0; l < D; ++l) xj[p][l] = xn[p][l];
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (!valid[p]) continue;
+        if (bad[p]) {
+            record_error(a.err_flags, QRMC_ESIM, bad[p]);
+        } else {
+            const double term = terminal<D>(a.prob, xj[p]);
+            const double v = DDIV(DADD(term, DMUL(a.dt, dsum[p])), w0[p]);
+            if (!isfinite(v)) record_error(a.err_flags, QRMC_ENUMERIC, 0);
+            a.resp[q[p]] = v;
         }
     }
     // truncation counters: warp-aggregate then one atomic per warp
@@ -234,23 +282,27 @@ __global__ void k_stream_draws(uint64_t seed, const uint64_t* sids, int64_t n, i
     }
 }
 
+template <int D>
 __global__ void k_cloud_paths(const StepArgs a, int64_t first, int64_t n, double* out, int* bad_out) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    const int d = a.prob.dim;
-    const int64_t len = static_cast<int64_t>(a.steps - a.step + 1) * d;
+    const int64_t len = static_cast<int64_t>(a.steps - a.step + 1) * D;
     double* path = out + r * len;
     Stream s(a.seed, sid_training(a.step, static_cast<uint64_t>(first + r)));
-    double x[kMaxDim];
-    sample_start(a.meas, d, s, x);
-    for (int l = 0; l < d; ++l) path[l] = x[l];
+    double x[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        x[l] = measure_inv_cdf(a.meas, s.next_uniform(), l);
+        path[l] = x[l];
+    }
     for (int j = a.step; j < a.steps; ++j) {
-        const int b = euler_step(a.prob, x, a.sqrt_dt, a.dt, s, j);
+        const int b = euler_step<D>(a.prob, x, a.sqrt_dt, a.dt, s, j);
         if (b) {
             atomicMax(bad_out, b);
             return;
         }
-        for (int l = 0; l < d; ++l) path[(j + 1 - a.step) * d + l] = x[l];
+#pragma unroll
+        for (int l = 0; l < D; ++l) path[(j + 1 - a.step) * D + l] = x[l];
     }
 }
 
@@ -263,7 +315,7 @@ __global__ void k_eval_points(const StepArgs a, const double* alpha_row, const d
 #pragma unroll
     for (int l = 0; l < D; ++l) p[l] = x[r * D + l];
     const double y = eval_at<D>(a, alpha_row, p);
-    out[r] = with_weight ? DMUL(y, damping_weight(p, D, q)) : y;
+    out[r] = with_weight ? DMUL(y, damping_weight<D>(p, q)) : y;
 }
 
 // mse_metrics (benchmark.cpp:86-151): per (step i, point m) squared errors of
@@ -277,34 +329,37 @@ __global__ void k_mse(const StepArgs a, double kappa, double lam, double horizon
     Stream s(eval_seed, sid_evaluation(i, static_cast<uint64_t>(r)));
     double p[D];
     sample_start(a.meas, D, s, p);
-    const double w = damping_weight(p, D, a.q);
+    const double w = damping_weight<D>(p, a.q);
     const double approx = eval_at<D>(a, a.alpha_packed + static_cast<int64_t>(i) * a.kp, p);
     const double t = DMUL(static_cast<double>(i), a.dt);
     const double e_exp = exp(DDIV(DMUL(DMUL(DMUL(lam, lam), static_cast<double>(D)), DSUB(t, horizon)), 2.0));
-    const double truth = DADD(DADD(1.0, kappa), DMUL(sin(DMUL(lam, sum_of(p, D))), e_exp));
+    const double truth = DADD(DADD(1.0, kappa), DMUL(sin(DMUL(lam, sum_of<D>(p))), e_exp));
     const double e = DSUB(approx, DDIV(truth, w));
     sq[static_cast<int64_t>(i) * eval_points + r] = DMUL(e, e);
     sq_u[static_cast<int64_t>(i) * eval_points + r] = DMUL(DMUL(DMUL(e, e), w), w);
 }
 
 // ---------------------------------------------------------------- dispatch
-#define QRMC_DISPATCH_D(dim, CALL)                  \
+#define QRMC_DISPATCH_D(dim, ...)                  \
     switch (dim) {                                  \
-        case 1: { constexpr int D = 1; CALL; } break; \
-        case 2: { constexpr int D = 2; CALL; } break; \
-        case 3: { constexpr int D = 3; CALL; } break; \
-        case 4: { constexpr int D = 4; CALL; } break; \
-        case 5: { constexpr int D = 5; CALL; } break; \
-        case 6: { constexpr int D = 6; CALL; } break; \
-        case 7: { constexpr int D = 7; CALL; } break; \
-        case 8: { constexpr int D = 8; CALL; } break; \
+        case 1: { constexpr int D = 1; __VA_ARGS__; } break; \
+        case 2: { constexpr int D = 2; __VA_ARGS__; } break; \
+        case 3: { constexpr int D = 3; __VA_ARGS__; } break; \
+        case 4: { constexpr int D = 4; __VA_ARGS__; } break; \
+        case 5: { constexpr int D = 5; __VA_ARGS__; } break; \
+        case 6: { constexpr int D = 6; __VA_ARGS__; } break; \
+        case 7: { constexpr int D = 7; __VA_ARGS__; } break; \
+        case 8: { constexpr int D = 8; __VA_ARGS__; } break; \
         default: return cudaErrorInvalidValue;      \
     }
 
-cudaError_t launch_responses(const StepArgs& a, cudaStream_t st) {
+cudaError_t launch_responses(const StepArgs& a, const SeriesTiles& t, cudaStream_t st) {
     if (a.n_owned == 0) return cudaSuccess;
-    const unsigned blocks = static_cast<unsigned>((a.n_owned + 127) / 128);
-    QRMC_DISPATCH_D(a.prob.dim, (k_responses<D><<<blocks, 128, 0, st>>>(a)));
+    QRMC_DISPATCH_D(a.prob.dim, {
+        const int64_t per_cta = static_cast<int64_t>(kK1Threads) * K1Shape<D>::P;
+        const unsigned blocks = static_cast<unsigned>((a.n_owned + per_cta - 1) / per_cta);
+        k_responses<D><<<blocks, kK1Threads, 0, st>>>(a, t);
+    });
     return cudaGetLastError();
 }
 
@@ -353,7 +408,7 @@ cudaError_t launch_stream_draws(uint64_t seed, const uint64_t* sids, int64_t n, 
 cudaError_t launch_cloud_paths(const StepArgs& a, int64_t first, int64_t n, double* out, int* bad,
                                cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>((n + 127) / 128);
-    k_cloud_paths<<<blocks, 128, 0, st>>>(a, first, n, out, bad);
+    QRMC_DISPATCH_D(a.prob.dim, (k_cloud_paths<D><<<blocks, 128, 0, st>>>(a, first, n, out, bad)));
     return cudaGetLastError();
 }
 

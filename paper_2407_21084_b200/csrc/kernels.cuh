@@ -9,6 +9,14 @@
 #include "qrmc_types.h"
 
 namespace qrmc_dev {
+struct SeriesTiles {
+    const int4* tiles;        // {prog_off (16-byte aligned), n_runs, alpha_off (even), alpha_len (even)}
+    int n_tiles;
+    const uint32_t* prog;     // per-tile segments
+};
+}  // namespace qrmc_dev
+
+namespace qrmc_dev {
 
 constexpr int kTermsPerThread = 2;
 
@@ -55,7 +63,7 @@ struct FinishArgs {
     const double* pack_scale;    // sqrt2^{nnz(k)}
 };
 
-cudaError_t launch_responses(const StepArgs& a, cudaStream_t st);
+cudaError_t launch_responses(const StepArgs& a, const SeriesTiles& t, cudaStream_t st);
 size_t project_smem_bytes(const ProjArgs& p);
 cudaError_t configure_project(int dim, size_t smem);
 cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st);

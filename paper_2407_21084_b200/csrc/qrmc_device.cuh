@@ -53,6 +53,7 @@ struct Stream {
     uint64_t buf1;
     int pos;  // 0: buf empty, 1: buf1 holds the second half
 
+    __device__ __forceinline__ Stream() : key(make_uint2(0u, 0u)), sid_lo(0), sid_hi(0), block(0), buf1(0), pos(0) {}
     __device__ __forceinline__ Stream(uint64_t seed, uint64_t sid)
         : key(make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32))),
           sid_lo(static_cast<uint32_t>(sid)), sid_hi(static_cast<uint32_t>(sid >> 32)),
@@ -115,21 +116,27 @@ __device__ __forceinline__ double measure_inv_cdf(const MeasureDev& m, double u,
 // (sde.hpp:23-29; SinBenchmark functors benchmark.cpp:46-62).
 
 
-__device__ __forceinline__ double sum_of(const double* x, int d) {
+// All functors take the state dimension D as a template parameter so every
+// per-coordinate loop unrolls and point arrays stay in registers.
+template <int D>
+__device__ __forceinline__ double sum_of(const double* x) {
     double s = 0.0;
-    for (int l = 0; l < d; ++l) s = DADD(s, x[l]);
+#pragma unroll
+    for (int l = 0; l < D; ++l) s = DADD(s, x[l]);
     return s;
 }
 
+template <int D>
 __device__ __forceinline__ double terminal(const ProblemDev& p, const double* x) {
     switch (p.terminal_kind) {
-        case QRMC_TERMINAL_SIN_SUM: return DADD(DADD(1.0, p.tp0), sin(DMUL(p.tp1, sum_of(x, p.dim))));
+        case QRMC_TERMINAL_SIN_SUM: return DADD(DADD(1.0, p.tp0), sin(DMUL(p.tp1, sum_of<D>(x))));
         case QRMC_TERMINAL_CONST: return p.tp0;
         case QRMC_TERMINAL_X0: return x[0];
         default: return DDIV(1.0, DSUB(x[0], x[0]));
     }
 }
 
+template <int D>
 __device__ __forceinline__ double driver(const ProblemDev& p, double t, const double* x, double y) {
     switch (p.driver_kind) {
         case QRMC_DRIVER_ZERO: return 0.0;
@@ -137,9 +144,9 @@ __device__ __forceinline__ double driver(const ProblemDev& p, double t, const do
         case QRMC_DRIVER_Y: return y;
         default: {
             // y - kappa - 1 - sin(lam sum x) * exp(lam*lam*d*(t-T)/2)  (benchmark.cpp:57-61)
-            const double e = exp(DDIV(DMUL(DMUL(DMUL(p.dp1, p.dp1), static_cast<double>(p.dim)),
+            const double e = exp(DDIV(DMUL(DMUL(DMUL(p.dp1, p.dp1), static_cast<double>(D)),
                                            DSUB(t, p.horizon)), 2.0));
-            const double z = DSUB(DSUB(DSUB(y, p.dp0), 1.0), DMUL(sin(DMUL(p.dp1, sum_of(x, p.dim))), e));
+            const double z = DSUB(DSUB(DSUB(y, p.dp0), 1.0), DMUL(sin(DMUL(p.dp1, sum_of<D>(x))), e));
             const double zz = DMUL(z, z);
             return zz < 1.0 ? zz : 1.0;
         }
@@ -147,18 +154,22 @@ __device__ __forceinline__ double driver(const ProblemDev& p, double t, const do
 }
 
 // lstar_bound (sde.cpp:27-35)
+template <int D>
 __device__ __forceinline__ double lstar(const ProblemDev& p, const double* x) {
     if (p.eta == 0.0) return p.lstar_base;
     double n2 = 0.0;
-    for (int l = 0; l < p.dim; ++l) n2 = DADD(n2, DMUL(x[l], x[l]));
+#pragma unroll
+    for (int l = 0; l < D; ++l) n2 = DADD(n2, DMUL(x[l], x[l]));
     return DMUL(p.lstar_base, pow(DADD(1.0, n2), DDIV(p.eta, 2.0)));
 }
 
 // damping_weight (solver.cpp:43-48)
-__device__ __forceinline__ double damping_weight(const double* x, int d, double q) {
+template <int D>
+__device__ __forceinline__ double damping_weight(const double* x, double q) {
     if (q == 0.0) return 1.0;
     double n2 = 0.0;
-    for (int l = 0; l < d; ++l) n2 = DADD(n2, DMUL(x[l], x[l]));
+#pragma unroll
+    for (int l = 0; l < D; ++l) n2 = DADD(n2, DMUL(x[l], x[l]));
     return pow(DADD(1.0, n2), DDIV(q, 2.0));
 }
 
@@ -169,13 +180,17 @@ __device__ __forceinline__ double truncate_soft(double v, double b) {
     return b < v ? b : v;
 }
 
-// euler_step in place (sde.cpp:37-73). Returns 0 or the SimulationError step.
+// euler_step in place (sde.cpp:37-73); device diffusions have brownian_dim == D.
+// Returns 0 or the SimulationError step.
+template <int D>
 __device__ __forceinline__ int euler_step(const ProblemDev& p, double* x, double sqrt_dt, double dt,
                                           Stream& s, int j) {
-    double dw[kMaxDim];
-    for (int l = 0; l < p.bdim; ++l) dw[l] = DMUL(sqrt_dt, s.next_normal());
+    double dw[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) dw[l] = DMUL(sqrt_dt, s.next_normal());
     int bad = 0;
-    for (int l = 0; l < p.dim; ++l) {
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
         const double out = p.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(p.sigma, dw[l]) : dw[l];
         double v;
         if (p.drift_kind == QRMC_DRIFT_CONST)
