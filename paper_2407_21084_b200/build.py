@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}",
            *map(str, SOURCES), "-o", str(tmp), "-ldl"]
     if verbose:

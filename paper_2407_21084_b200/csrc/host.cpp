@@ -179,20 +179,93 @@ Gamma build_gamma(int kind, int dim, const int32_t* degrees, int n_degrees) {
 
 // Trie node program + packed layout (see series_eval in qrmc_device.cuh).
 struct Program {
-    std::vector<uint32_t> prog;
-    std::vector<int32_t> pack_pos;
-    std::vector<double> pack_scale;
-    int64_t kp = 0;
-    // shared-memory tiles of the program (series_block.cuh)
-    std::vector<int4> tiles;
-    std::vector<uint32_t> tile_prog;
+    std::vector<int32_t> pack_pos;   // k -> position in the packed row
+    std::vector<double> pack_scale;  // sqrt2^{nnz(k)}
+    int64_t kp = 0;                  // packed row length (even)
+    std::vector<int4> tiles;         // shared-memory tiles (series_block.cuh)
+    std::vector<uint32_t> tile_prog; // group program, per-tile 16-byte aligned segments
 };
 
 constexpr int kHostTileA = 2048;  // == kTileA in series_block.cuh
 constexpr int kHostTileP = 1024;  // == kTileP
-constexpr uint32_t kFirstRunCode = 15;
+constexpr uint32_t kFirstGroupCode = 15, kContGroupCode = 14;
 
-void build_tiles(Program& p) {
+// Group program of series_block.cuh: one group per upper prefix (k_0..k_{D-3}),
+// holding the leaf-run lengths of its siblings k_{D-2} = 0..n-1, cut into
+// shared-memory tiles. Verifies downward closure on the way (lexicographic
+// order of a downward-closed set advances exactly one level by one and resets
+// the deeper ones).
+Program build_program(const Gamma& g) {
+    Program p;
+    const int d = g.dim;
+    const int64_t K = g.size();
+    const int S2 = k1_s2(d);
+    p.pack_pos.resize(static_cast<size_t>(K));
+    p.pack_scale.resize(static_cast<size_t>(K));
+    auto at = [&](int64_t i, int l) { return g.rows[static_cast<size_t>(i * d + l)]; };
+
+    // 1. leaf runs and their packed positions
+    struct Run { int64_t first; int64_t R; };
+    std::vector<Run> runs;
+    int64_t pos = 0;
+    for (int64_t i = 0; i < K;) {
+        int64_t j = i;
+        auto same = [&](int64_t r) {
+            for (int l = 0; l < d - 1; ++l)
+                if (at(r, l) != at(i, l)) return false;
+            return true;
+        };
+        while (j < K && same(j)) {
+            if (at(j, d - 1) != j - i) fail(QRMC_ELOGIC, "index set is not downward closed (leaf run)");
+            ++j;
+        }
+        runs.push_back({i, j - i});
+        for (int64_t b = 0; b < j - i; ++b) {
+            int nnz = 0;
+            for (int l = 0; l < d; ++l) nnz += at(i + b, l) != 0;
+            double s = std::ldexp(1.0, nnz / 2);
+            if (nnz & 1) s *= 1.4142135623730951;
+            p.pack_pos[static_cast<size_t>(i + b)] = static_cast<int32_t>(pos + b);
+            p.pack_scale[static_cast<size_t>(i + b)] = s;
+        }
+        pos += (j - i + 1) & ~int64_t{1};
+        i = j;
+    }
+    p.kp = std::max<int64_t>(pos, 2);
+
+    // 2. groups of sibling runs under one upper prefix
+    struct Group { size_t r0, n; uint32_t L; };
+    std::vector<Group> groups;
+    const int nu = std::max(d - 2, 0);  // upper levels 0..d-3
+    for (size_t r = 0; r < runs.size();) {
+        size_t e = r;
+        auto same_upper = [&](size_t q) {
+            for (int l = 0; l < nu; ++l)
+                if (at(runs[q].first, l) != at(runs[r].first, l)) return false;
+            return true;
+        };
+        while (e < runs.size() && same_upper(e)) {
+            if (d >= 2 && at(runs[e].first, d - 2) != static_cast<int32_t>(e - r))
+                fail(QRMC_ELOGIC, "index set is not downward closed (siblings)");
+            ++e;
+        }
+        uint32_t L = kFirstGroupCode;
+        if (!groups.empty()) {
+            const int64_t a = runs[groups.back().r0].first, b = runs[r].first;
+            int l = 0;
+            while (l < nu && at(a, l) == at(b, l)) ++l;
+            if (l >= nu || at(b, l) != at(a, l) + 1) fail(QRMC_ELOGIC, "index set is not downward closed (groups)");
+            for (int t = l + 1; t < nu; ++t)
+                if (at(b, t) != 0) fail(QRMC_ELOGIC, "index set is not downward closed (reset)");
+            L = static_cast<uint32_t>(l);
+        }
+        if (e - r >= (1u << 14)) fail(QRMC_ENOTIMPL, "too many sibling runs in one group");
+        groups.push_back({r, e - r, L});
+        r = e;
+    }
+
+    // 3. tiles: a group chunk never splits a run; the first chunk of a group holds
+    // at least its first min(n, S2) siblings (the register-table part)
     int4 cur = make_int4(0, 0, 0, 0);
     int64_t alpha_pos = 0;
     auto close = [&] {
@@ -200,72 +273,39 @@ void build_tiles(Program& p) {
         p.tiles.push_back(cur);
         while (p.tile_prog.size() % 4) p.tile_prog.push_back(0);
     };
-    for (uint32_t w : p.prog) {
-        const int64_t R = w >> 4;
-        const int64_t padded = (R + 1) & ~int64_t{1};
-        if (padded > kHostTileA) fail(QRMC_ENOTIMPL, fmt("leaf run of %lld coefficients exceeds a tile", (long long)R));
-        if (cur.y == kHostTileP || cur.w + padded > kHostTileA) {
-            close();
-            cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0);
+    auto open = [&] { cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0); };
+    auto padded = [&](size_t r) { return (runs[r].R + 1) & ~int64_t{1}; };
+    open();
+    for (const Group& gr : groups) {
+        size_t s = 0;
+        while (s < gr.n) {
+            // the minimum this chunk must hold
+            const size_t need = s == 0 ? std::min<size_t>(gr.n, static_cast<size_t>(S2)) : 1;
+            int64_t need_a = 0;
+            for (size_t q = 0; q < need; ++q) need_a += padded(gr.r0 + s + q);
+            if (need_a > kHostTileA || static_cast<int64_t>(need) + 1 > kHostTileP)
+                fail(QRMC_ENOTIMPL, "a sibling group exceeds a shared-memory tile");
+            if (cur.w + need_a > kHostTileA || cur.y + static_cast<int64_t>(need) + 1 > kHostTileP) {
+                close();
+                open();
+            }
+            size_t take = need;
+            int64_t take_a = need_a;
+            while (s + take < gr.n && cur.w + take_a + padded(gr.r0 + s + take) <= kHostTileA &&
+                   cur.y + static_cast<int64_t>(take) + 2 <= kHostTileP) {
+                take_a += padded(gr.r0 + s + take);
+                ++take;
+            }
+            const uint32_t L = s == 0 ? gr.L : kContGroupCode;
+            p.tile_prog.push_back(L | (static_cast<uint32_t>(take) << 4) | (static_cast<uint32_t>(s) << 18));
+            for (size_t q = 0; q < take; ++q) p.tile_prog.push_back(static_cast<uint32_t>(runs[gr.r0 + s + q].R));
+            cur.y += static_cast<int>(take) + 1;
+            cur.w += static_cast<int>(take_a);
+            alpha_pos += take_a;
+            s += take;
         }
-        if (cur.y == 0) cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0);
-        p.tile_prog.push_back(w);
-        cur.y += 1;
-        cur.w += static_cast<int>(padded);
-        alpha_pos += padded;
     }
     close();
-}
-
-Program build_program(const Gamma& g) {
-    Program p;
-    const int d = g.dim;
-    const int64_t K = g.size();
-    p.pack_pos.resize(static_cast<size_t>(K));
-    p.pack_scale.resize(static_cast<size_t>(K));
-    int64_t pos = 0;
-    int64_t i = 0;
-    std::vector<int32_t> prev_prefix;
-    while (i < K) {
-        const int32_t* row = &g.rows[static_cast<size_t>(i * d)];
-        int64_t j = i;
-        auto same_prefix = [&](int64_t r) {
-            for (int l = 0; l < d - 1; ++l)
-                if (g.rows[static_cast<size_t>(r * d + l)] != row[l]) return false;
-            return true;
-        };
-        while (j < K && same_prefix(j)) {
-            if (g.rows[static_cast<size_t>(j * d + d - 1)] != j - i)
-                fail(QRMC_ELOGIC, "index set is not downward closed (leaf run)");
-            ++j;
-        }
-        const int64_t R = j - i;
-        int L = static_cast<int>(kFirstRunCode);
-        if (i > 0) {
-            L = 0;
-            while (L < d - 1 && prev_prefix[L] == row[L]) ++L;
-            if (L >= d - 1 || row[L] != prev_prefix[L] + 1)
-                fail(QRMC_ELOGIC, "index set is not downward closed (node transition)");
-            for (int l = L + 1; l < d - 1; ++l)
-                if (row[l] != 0) fail(QRMC_ELOGIC, "index set is not downward closed (reset)");
-        }
-        if (L > 15 || R >= (int64_t{1} << 28)) fail(QRMC_ENOTIMPL, "index set too deep for the node program");
-        p.prog.push_back(static_cast<uint32_t>(L) | (static_cast<uint32_t>(R) << 4));
-        for (int64_t b = 0; b < R; ++b) {
-            const int32_t* r = &g.rows[static_cast<size_t>((i + b) * d)];
-            int nnz = 0;
-            for (int l = 0; l < d; ++l) nnz += r[l] != 0;
-            double s = std::ldexp(1.0, nnz / 2);
-            if (nnz & 1) s *= 1.4142135623730951;
-            p.pack_pos[static_cast<size_t>(i + b)] = static_cast<int32_t>(pos + b);
-            p.pack_scale[static_cast<size_t>(i + b)] = s;
-        }
-        pos += (R + 1) & ~int64_t{1};
-        prev_prefix.assign(row, row + std::max(d - 1, 0));
-        i = j;
-    }
-    p.kp = std::max<int64_t>(pos, 2);
-    build_tiles(p);
     return p;
 }
 
@@ -368,6 +408,19 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
 };
 
+// The series program on the device (tiles + group words).
+struct DevProgram {
+    DevBuf<int4> tiles;
+    DevBuf<uint32_t> prog;
+    DevProgram(const Program& p, cudaStream_t st) {
+        tiles.alloc(p.tiles.size());
+        tiles.upload(p.tiles.data(), p.tiles.size(), st);
+        prog.alloc(p.tile_prog.size());
+        prog.upload(p.tile_prog.data(), p.tile_prog.size(), st);
+    }
+    SeriesTiles view() const { return SeriesTiles{tiles.p, static_cast<int>(tiles.n), prog.p}; }
+};
+
 // ------------------------------------------------------------------ NCCL (loaded lazily)
 struct NcclApi {
     void* handle = nullptr;
@@ -424,7 +477,7 @@ struct qrmc_gpu_plan {
     int64_t K = 0;
     int steps = 0;
     int lanes_per_rank = kLanes;
-    DevBuf<uint32_t> d_prog, d_tile_prog;
+    DevBuf<uint32_t> d_tile_prog;
     DevBuf<int4> d_tiles;
     DevBuf<int32_t> d_rows, d_pack_pos;
     DevBuf<double> d_pack_scale, d_alpha, d_coef, d_partials, d_resp, d_cloud;
@@ -493,8 +546,7 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
     for (int i = N - 1; i >= 0; --i) {
         StepArgs a = P.base;
         a.step = i;
-        SeriesTiles t{P.d_tiles.p, static_cast<int>(P.d_tiles.n), P.d_tile_prog.p};
-        cuda_check(launch_responses(a, t, st), "k_responses");
+        cuda_check(launch_responses(a, st), "k_responses");
         mark();
         ProjArgs pa = P.proj;
         pa.partials = P.d_partials.p + static_cast<size_t>(P.session->rank) * P.lanes_per_rank * P.K;
@@ -545,8 +597,6 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
 
     // device tables
     const Program& pg = P->program;
-    P->d_prog.alloc(pg.prog.size());
-    P->d_prog.upload(pg.prog.data(), pg.prog.size(), st);
     P->d_tiles.alloc(pg.tiles.size());
     P->d_tiles.upload(pg.tiles.data(), pg.tiles.size(), st);
     P->d_tile_prog.alloc(pg.tile_prog.size());
@@ -583,8 +633,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     a.n_owned = n_owned;
     a.alpha_packed = P->d_alpha.p;
     a.kp = pg.kp;
-    a.prog = P->d_prog.p;
-    a.n_runs = static_cast<int>(pg.prog.size());
+    a.tiles = SeriesTiles{P->d_tiles.p, static_cast<int>(P->d_tiles.n), P->d_tile_prog.p};
     a.resp = P->d_resp.p;
     a.cloud = P->d_cloud.p;
     a.counters = P->d_counters.p;
@@ -611,7 +660,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     P->ev.resize(3 * static_cast<size_t>(cfg.steps) + 1);
     for (auto& e : P->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     P->launches_per_run = 3 * cfg.steps;
-    P->h2d_bytes = pg.prog.size() * sizeof(uint32_t) + P->gamma.rows.size() * sizeof(int32_t) +
+    P->h2d_bytes = P->gamma.rows.size() * sizeof(int32_t) +
                    pg.pack_pos.size() * sizeof(int32_t) + pg.pack_scale.size() * sizeof(double) +
                    pg.tiles.size() * sizeof(int4) + pg.tile_prog.size() * sizeof(uint32_t);
     P->d2h_bytes = static_cast<uint64_t>(cfg.steps) * P->K * sizeof(double) + 2 * sizeof(unsigned long long) +
@@ -902,12 +951,10 @@ qrmc_status qrmc_gpu_evaluate(const qrmc_config_t* config, int32_t dim, const do
         for (int64_t k = 0; k < g.size(); ++k) packed[pg.pack_pos[k]] = coeffs_step[k] * pg.pack_scale[k];
         DevBuf<double> d_alpha(packed.size()), d_x(static_cast<size_t>(std::max<int64_t>(n, 1)) * dim),
             d_out(static_cast<size_t>(std::max<int64_t>(n, 1)));
-        DevBuf<uint32_t> d_prog(pg.prog.size());
+        DevProgram dp(pg, st);
         d_alpha.upload(packed.data(), packed.size(), st);
-        d_prog.upload(pg.prog.data(), pg.prog.size(), st);
         if (n) d_x.upload(x, static_cast<size_t>(n) * dim, st);
-        a.prog = d_prog.p;
-        a.n_runs = static_cast<int>(pg.prog.size());
+        a.tiles = dp.view();
         if (n) cuda_check(launch_eval_points(a, d_alpha.p, d_x.p, n, config->damping, 1, d_out.p, st), "k_eval_points");
         cuda_check(cudaStreamSynchronize(st), "evaluate");
         if (n) cuda_check(cudaMemcpy(out, d_out.p, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
@@ -935,11 +982,9 @@ qrmc_status qrmc_gpu_mse_metrics(const qrmc_config_t* config, int32_t dim, doubl
                 packed[static_cast<size_t>(i) * pg.kp + pg.pack_pos[k]] = coeffs[static_cast<size_t>(i) * g.size() + k] * pg.pack_scale[k];
         DevBuf<double> d_alpha(packed.size()), d_sq(static_cast<size_t>(N) * eval_points),
             d_squ(static_cast<size_t>(N) * eval_points);
-        DevBuf<uint32_t> d_prog(pg.prog.size());
+        DevProgram dp(pg, st);
         d_alpha.upload(packed.data(), packed.size(), st);
-        d_prog.upload(pg.prog.data(), pg.prog.size(), st);
-        a.prog = d_prog.p;
-        a.n_runs = static_cast<int>(pg.prog.size());
+        a.tiles = dp.view();
         a.alpha_packed = d_alpha.p;
         a.kp = pg.kp;
         const double lam = prob.terminal_params[1];

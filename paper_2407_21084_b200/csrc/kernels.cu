@@ -41,34 +41,16 @@ __device__ __forceinline__ void sample_start(const MeasureDev& m, int d, Stream&
     for (int l = 0; l < d; ++l) x[l] = measure_inv_cdf(m, s.next_uniform(), l);
 }
 
-template <int D>
-__device__ __forceinline__ double eval_at(const StepArgs& a, const double* alpha_row, const double* x) {
-    double c1[D];
-#pragma unroll
-    for (int l = 0; l < D; ++l) c1[l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, x[l], l)));
-    return series_eval<D>(alpha_row, a.prog, a.n_runs, c1);
-}
-
 // ---------------------------------------------------------------- K1
 // P paths per thread, 128 threads per CTA; the CTA walks the backward step's
 // future time points in lockstep so that each coefficient row alpha_{j+1}
-// streams through shared memory once per CTA (series_block.cuh).
-template <int D>
-struct K1Shape;
-template <> struct K1Shape<1> { static constexpr int P = 4, LT = 16; };
-template <> struct K1Shape<2> { static constexpr int P = 2, LT = 32; };
-template <> struct K1Shape<3> { static constexpr int P = 2, LT = 16; };
-template <> struct K1Shape<4> { static constexpr int P = 2, LT = 8; };
-template <> struct K1Shape<5> { static constexpr int P = 2, LT = 8; };
-template <> struct K1Shape<6> { static constexpr int P = 2, LT = 8; };
-template <> struct K1Shape<7> { static constexpr int P = 1, LT = 8; };
-template <> struct K1Shape<8> { static constexpr int P = 1, LT = 8; };
-
+// streams through shared memory once per CTA (series_block.cuh). P, S2, LT
+// per dimension: k1_p / k1_s2 / k1_lt (qrmc_types.h).
 constexpr int kK1Threads = 128;
 
 template <int D>
-__global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a, const SeriesTiles st) {
-    constexpr int P = K1Shape<D>::P, LT = K1Shape<D>::LT;
+__global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
+    constexpr int P = k1_p(D), S2 = k1_s2(D), LT = k1_lt(D);
     __shared__ SeriesSmem sm;
     __shared__ int s_abort;
     if (threadIdx.x == 0) s_abort = *a.abort_flag;
@@ -117,7 +99,7 @@ __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a, cons
 #pragma unroll
                 for (int l = 0; l < D; ++l)
                     c1[p][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xn[p][l], l)));
-            series_block<D, P, LT>(sm, st, a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp, c1, ys);
+            series_block<D, P, S2, LT>(sm, a.tiles, a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp, c1, ys);
 #pragma unroll
             for (int p = 0; p < P; ++p) y[p] = DMUL(ys[p], damping_weight<D>(xn[p], a.q));
         }
@@ -306,31 +288,46 @@ __global__ void k_cloud_paths(const StepArgs a, int64_t first, int64_t n, double
     }
 }
 
+// evaluate_solution / SeriesEvaluator::eval at given points (solver.cpp:228-237),
+// one point per thread; every thread of the CTA joins the series walk.
 template <int D>
-__global__ void k_eval_points(const StepArgs a, const double* alpha_row, const double* x, int64_t n,
-                              double q, int with_weight, double* out) {
+__global__ void __launch_bounds__(kK1Threads) k_eval_points(const StepArgs a, const double* alpha_row,
+                                                            const double* x, int64_t n, double q,
+                                                            int with_weight, double* out) {
+    __shared__ SeriesSmem sm;
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    double p[D];
+    const int64_t rr = r < n ? r : n - 1;
+    double p[D], c1[1][D], y[1];
 #pragma unroll
-    for (int l = 0; l < D; ++l) p[l] = x[r * D + l];
-    const double y = eval_at<D>(a, alpha_row, p);
-    out[r] = with_weight ? DMUL(y, damping_weight<D>(p, q)) : y;
+    for (int l = 0; l < D; ++l) {
+        p[l] = x[rr * D + l];
+        c1[0][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, p[l], l)));
+    }
+    series_block<D, 1, k1_s2(D), k1_lt(D)>(sm, a.tiles, alpha_row, c1, y);
+    if (r < n) out[r] = with_weight ? DMUL(y[0], damping_weight<D>(p, q)) : y[0];
 }
 
 // mse_metrics (benchmark.cpp:86-151): per (step i, point m) squared errors of
 // the damped series against exact_solution/weight (benchmark.cpp:20-28).
 template <int D>
-__global__ void k_mse(const StepArgs a, double kappa, double lam, double horizon, uint64_t eval_seed,
-                      int eval_points, double* sq, double* sq_u) {
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kK1Threads) k_mse(const StepArgs a, double kappa, double lam, double horizon,
+                                                    uint64_t eval_seed, int eval_points, double* sq,
+                                                    double* sq_u) {
+    __shared__ SeriesSmem sm;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t r = r0 < eval_points ? r0 : eval_points - 1;
     const int i = blockIdx.y;
-    if (r >= eval_points) return;
     Stream s(eval_seed, sid_evaluation(i, static_cast<uint64_t>(r)));
-    double p[D];
-    sample_start(a.meas, D, s, p);
+    double p[D], c1[1][D], y[1];
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        p[l] = measure_inv_cdf(a.meas, s.next_uniform(), l);
+        c1[0][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, p[l], l)));
+    }
     const double w = damping_weight<D>(p, a.q);
-    const double approx = eval_at<D>(a, a.alpha_packed + static_cast<int64_t>(i) * a.kp, p);
+    series_block<D, 1, k1_s2(D), k1_lt(D)>(sm, a.tiles, a.alpha_packed + static_cast<int64_t>(i) * a.kp, c1, y);
+    if (r0 >= eval_points) return;
+    const double approx = y[0];
     const double t = DMUL(static_cast<double>(i), a.dt);
     const double e_exp = exp(DDIV(DMUL(DMUL(DMUL(lam, lam), static_cast<double>(D)), DSUB(t, horizon)), 2.0));
     const double truth = DADD(DADD(1.0, kappa), DMUL(sin(DMUL(lam, sum_of<D>(p))), e_exp));
@@ -353,12 +350,12 @@ __global__ void k_mse(const StepArgs a, double kappa, double lam, double horizon
         default: return cudaErrorInvalidValue;      \
     }
 
-cudaError_t launch_responses(const StepArgs& a, const SeriesTiles& t, cudaStream_t st) {
+cudaError_t launch_responses(const StepArgs& a, cudaStream_t st) {
     if (a.n_owned == 0) return cudaSuccess;
     QRMC_DISPATCH_D(a.prob.dim, {
-        const int64_t per_cta = static_cast<int64_t>(kK1Threads) * K1Shape<D>::P;
+        const int64_t per_cta = static_cast<int64_t>(kK1Threads) * k1_p(D);
         const unsigned blocks = static_cast<unsigned>((a.n_owned + per_cta - 1) / per_cta);
-        k_responses<D><<<blocks, kK1Threads, 0, st>>>(a, t);
+        k_responses<D><<<blocks, kK1Threads, 0, st>>>(a);
     });
     return cudaGetLastError();
 }

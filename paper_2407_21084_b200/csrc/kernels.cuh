@@ -9,16 +9,15 @@
 #include "qrmc_types.h"
 
 namespace qrmc_dev {
-struct SeriesTiles {
-    const int4* tiles;        // {prog_off (16-byte aligned), n_runs, alpha_off (even), alpha_len (even)}
-    int n_tiles;
-    const uint32_t* prog;     // per-tile segments
-};
-}  // namespace qrmc_dev
-
-namespace qrmc_dev {
 
 constexpr int kTermsPerThread = 2;
+
+// Series program in device memory (series_block.cuh).
+struct SeriesTiles {
+    const int4* tiles;     // {prog_off (16-byte aligned), n_words, alpha_off (even), alpha_len (even)}
+    int n_tiles;
+    const uint32_t* prog;  // group words, per-tile segments
+};
 
 // Everything one backward step's kernels read (passed by value: it lives in
 // the kernel parameter space, so it is captured verbatim into CUDA graphs).
@@ -33,10 +32,9 @@ struct StepArgs {
     int lane_lo;          // this rank's lanes [lane_lo, lane_lo + owned_lanes)
     int owned_lanes;
     int64_t n_owned;      // paths owned by this rank
-    double* alpha_packed; // [N][kp] packed alpha' rows (series_eval layout)
+    double* alpha_packed; // [N][kp] packed alpha' rows (series_block layout)
     int64_t kp;
-    const uint32_t* prog; // trie node program, n_runs words
-    int n_runs;
+    SeriesTiles tiles;    // the series program
     double* resp;         // [n_owned]
     double* cloud;        // [dim][n_owned] (store mode) or nullptr (recompute)
     unsigned long long* counters;  // {applications, clipped}
@@ -63,7 +61,7 @@ struct FinishArgs {
     const double* pack_scale;    // sqrt2^{nnz(k)}
 };
 
-cudaError_t launch_responses(const StepArgs& a, const SeriesTiles& t, cudaStream_t st);
+cudaError_t launch_responses(const StepArgs& a, cudaStream_t st);
 size_t project_smem_bytes(const ProjArgs& p);
 cudaError_t configure_project(int dim, size_t smem);
 cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st);

@@ -203,91 +203,4 @@ __device__ __forceinline__ int euler_step(const ProblemDev& p, double* x, double
     return bad;
 }
 
-// ------------------------------------------------------------------ series
-// Student-cosine series  y(x) = sum_k alpha_k prod_l T_l[k_l]
-// (cosine_basis.cpp:67-112), evaluated by sum factorisation over Gamma's
-// lexicographic trie. The host packs alpha'_k = alpha_k * sqrt2^{nnz(k)} so
-// the device works with plain Chebyshev values c_l[v] = cos(v * pi * u_l)
-// (T_l[v] = sqrt2 c_l[v] for v >= 1, T_l[0] = c_l[0] = 1). The node program
-// holds one word per leaf run: bits 0..3 = level L whose index advanced
-// from the previous run (deeper levels reset to 0; lexicographic order of a
-// downward-closed set guarantees exactly this transition), bits 4.. = run
-// length R (leaf indices 0..R-1). Runs are padded to even length in alpha'.
-//
-// Horner over the trie: acc[l] accumulates sum_v c_l[v] V(prefix + v) for
-// the current prefix of length l; a finished run folds into acc[D-2], a
-// finished level-l node folds into acc[l-1].
-template <int D>
-__device__ __forceinline__ double series_eval(const double* __restrict__ alpha,
-                                              const uint32_t* __restrict__ prog, int n_runs,
-                                              const double (&c1)[D]) {
-    double two_c1[D], cur[D], prev[D];
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-        two_c1[l] = 2.0 * c1[l];
-        cur[l] = 1.0;
-        prev[l] = c1[l];  // c_{-1} = c_1: the recurrence then yields c_1 = 2 c1 * 1 - c1 = c1 exactly
-    }
-    constexpr int NA = D > 1 ? D - 1 : 1;
-    double acc[NA];
-#pragma unroll
-    for (int l = 0; l < NA; ++l) acc[l] = 0.0;
-    double y = 0.0;
-    const double2* a2 = reinterpret_cast<const double2*>(alpha);
-    for (int n = 0; n < n_runs; ++n) {
-        const uint32_t w = __ldg(prog + n);
-        const int L = static_cast<int>(w & 15u);
-        const int R = static_cast<int>(w >> 4);
-        if constexpr (D >= 2) {
-            if (n > 0) {
-                // close levels L+1..D-2 (fold into the parent), then advance level L
-#pragma unroll
-                for (int l = D - 3; l >= 0; --l) {
-                    if (l >= L) {
-                        acc[l] = fma(cur[l], acc[l + 1], acc[l]);
-                        acc[l + 1] = 0.0;
-                    }
-                }
-#pragma unroll
-                for (int l = 0; l < D - 1; ++l) {
-                    if (l == L) {
-                        const double nx = fma(two_c1[l], cur[l], -prev[l]);
-                        prev[l] = cur[l];
-                        cur[l] = nx;
-                    } else if (l > L) {
-                        cur[l] = 1.0;
-                        prev[l] = c1[l];
-                    }
-                }
-            }
-        }
-        // leaf run: s = sum_{b<R} alpha'[b] c_{D-1}[b]
-        double s0 = 0.0, s1 = 0.0;
-        double cp = c1[D - 1], cc = 1.0;
-        const double tc = two_c1[D - 1];
-        const int pairs = (R + 1) >> 1;
-        for (int b = 0; b < pairs; ++b) {
-            const double2 a = __ldg(a2 + b);
-            const double cn = fma(tc, cc, -cp);
-            s0 = fma(a.x, cc, s0);
-            s1 = fma(a.y, cn, s1);
-            const double c2 = fma(tc, cn, -cc);
-            cp = cn;  // (cp, cc) = (c_{2b+1}, c_{2b+2})
-            cc = c2;
-        }
-        a2 += pairs;
-        const double s = s0 + s1;
-        if constexpr (D >= 2)
-            acc[D - 2] = fma(cur[D - 2], s, acc[D - 2]);
-        else
-            y += s;
-    }
-    if constexpr (D >= 2) {
-#pragma unroll
-        for (int l = D - 3; l >= 0; --l) acc[l] = fma(cur[l], acc[l + 1], acc[l]);
-        y = acc[0];
-    }
-    return y;
-}
-
 }  // namespace qrmc_dev

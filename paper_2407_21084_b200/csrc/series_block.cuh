@@ -2,20 +2,29 @@
 //     y(x) = sum_{k in Gamma} alpha_k prod_l T_l[k_l](x)       (cosine_basis.cpp:67-112)
 // for P points per thread, all threads of a CTA on the same coefficient row.
 //
-// Layout (built by host.cpp): the packed row alpha'_k = alpha_k sqrt2^{nnz(k)}
-// in lexicographic (= depth-first trie) order, each leaf run padded to even
-// length; the node program (one word per leaf run: bits 0..3 transition
-// level L, 15 = first run of the set; bits 4.. run length R) cut into tiles
-// of <= kTileA coefficients and <= kTileP runs, never splitting a run.
-// Tiles stream HBM/L2 -> shared memory with cp.async, double-buffered, so
-// the inner loops read coefficients as 16-byte shared-memory broadcasts.
+// Sum factorisation over Gamma's lexicographic trie. With c_l[v] = cos(v pi u_l)
+// and alpha'_k = alpha_k sqrt2^{nnz(k)} (packed by host.cpp):
+//     y = sum_{upper prefix} (prod_{l<D-2} c_l) sum_s c_{D-2}[s] sum_b alpha'[.., s, b] c_{D-1}[b]
+// The two deepest levels are evaluated from per-point REGISTER tables,
+// c_{D-2}[0..S2) and c_{D-1}[0..LT), computed once per evaluation, so every
+// term inside the tables costs exactly one FMA and every leaf run one more
+// (its fold into the sibling sum). Indices beyond the tables continue the
+// reference's three-term Chebyshev recurrence (cosine_basis.cpp:79-86) in
+// registers. Levels above D-2 ("upper" levels) change rarely and carry
+// (2c1, c_prev, c_cur, acc) recurrence state.
 //
-// Per point the evaluation is sum factorisation over the trie (Horner on
-// every level): the leaf level uses a register table of the first LT
-// Chebyshev values c_b = cos(b pi u) (one FMA per term), runs longer than LT
-// continue the three-term recurrence in registers; internal levels carry
-// (c_prev, c_cur, 2c1, acc) in registers. Control flow is uniform across
-// the CTA (every thread walks the same program), so branches never diverge.
+// Program (host.cpp build_program): one GROUP per upper prefix (k_0..k_{D-3}),
+//   word 0: bits 0..3  transition level L of the upper prefix vs the previous
+//                      group (kFirstGroup for the first, kContGroup when the
+//                      group continues from the previous tile),
+//           bits 4..17 number of sibling runs n in this chunk,
+//           bits 18..31 first sibling index s0 (0, or >= S2 for continuations)
+//   words 1..n: leaf run lengths R_s (leaf indices 0..R_s-1)
+// and the packed coefficients of each run, padded to even length. Groups are
+// cut into tiles (<= kTileA coefficients, <= kTileP words) that stream
+// through shared memory with cp.async double buffering; inner loops read
+// coefficients as 16-byte shared-memory broadcasts. Control flow is uniform
+// across the CTA (every thread walks the same program), so it never diverges.
 #pragma once
 
 #include <cstdint>
@@ -24,10 +33,10 @@
 
 namespace qrmc_dev {
 
-constexpr int kTileA = 2048;  // coefficients per shared-memory tile (16 KiB)
-constexpr int kTileP = 1024;  // run words per tile (4 KiB)
-constexpr int kFirstRun = 15; // transition code of a set's first run
-
+constexpr int kTileA = 2048;    // coefficients per shared-memory tile (16 KiB)
+constexpr int kTileP = 1024;    // program words per tile (4 KiB)
+constexpr int kFirstGroup = 15; // transition code of the first group
+constexpr int kContGroup = 14;  // continuation of the previous tile's group
 
 struct SeriesSmem {
     double alpha[2][kTileA];
@@ -53,31 +62,82 @@ __device__ __forceinline__ void load_tile(SeriesSmem& sm, int buf, const SeriesT
     for (int c = threadIdx.x; c < np; c += blockDim.x) cp_async16(&sm.prog[buf][4 * c], gp + 4 * c);
 }
 
+// Leaf run z = sum_{b<R} alpha'[b] c_b for P points; pa advances past the run.
+template <int P, int LT>
+__device__ __forceinline__ void leaf_run(const double2*& pa, int R, const double (&leaf)[P][LT],
+                                         const double (&tl)[P], double (&z0)[P], double (&z1)[P]) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) z0[p] = z1[p] = 0.0;
+#pragma unroll
+    for (int b2 = 0; b2 < LT / 2; ++b2) {
+        if (2 * b2 < R) {
+            const double2 a = pa[b2];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                z0[p] = fma(a.x, leaf[p][2 * b2], z0[p]);
+                z1[p] = fma(a.y, leaf[p][2 * b2 + 1], z1[p]);
+            }
+        }
+    }
+    if (R > LT) {
+        double cp[P], cc[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            cp[p] = leaf[p][LT - 2];
+            cc[p] = leaf[p][LT - 1];
+        }
+        const int pairs = (R + 1) >> 1;
+        for (int b2 = LT / 2; b2 < pairs; ++b2) {
+            const double2 a = pa[b2];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const double e = fma(tl[p], cc[p], -cp[p]);  // c_{2 b2}
+                const double o = fma(tl[p], e, -cc[p]);      // c_{2 b2 + 1}
+                z0[p] = fma(a.x, e, z0[p]);
+                z1[p] = fma(a.y, o, z1[p]);
+                cp[p] = e;
+                cc[p] = o;
+            }
+        }
+    }
+    pa += (R + 1) >> 1;
+}
+
 // Evaluate the series of coefficient row `row` at P points per thread.
 // c1[p][l] = cos(pi u_l) of point p. Must be called by every thread of the CTA.
-template <int D, int P, int LT>
+template <int D, int P, int S2, int LT>
 __device__ __forceinline__ void series_block(SeriesSmem& sm, const SeriesTiles& st, const double* row,
                                              const double (&c1)[P][D], double (&y)[P]) {
-    static_assert(LT % 2 == 0 && LT >= 2, "leaf table holds pairs");
-    constexpr int NI = D > 1 ? D - 1 : 1;  // internal levels 0..D-2
-    double tc[P][NI], cur[P][NI], prev[P][NI], acc[P][NI];
-    double leaf[P][LT];
+    static_assert(LT % 2 == 0 && LT >= 2 && S2 >= 2, "table sizes");
+    constexpr int NU = D > 2 ? D - 2 : 1;  // upper levels 0..D-3
+    double utc[P][NU], ucur[P][NU], uprev[P][NU], uacc[P][NU];
+    double t2[P][S2], leaf[P][LT], tl[P], t2c[P];
+    double acc2[P], g2p[P], g2c[P];  // sibling sum of the current group; recurrence past S2
 #pragma unroll
     for (int p = 0; p < P; ++p) {
 #pragma unroll
-        for (int l = 0; l < NI; ++l) {
-            const double c = D > 1 ? c1[p][l] : 0.0;
-            tc[p][l] = 2.0 * c;
-            cur[p][l] = 1.0;
-            prev[p][l] = c;  // c_{-1} = c_1, so the first advance yields c_1 exactly
-            acc[p][l] = 0.0;
+        for (int l = 0; l < NU; ++l) {
+            const double c = D > 2 ? c1[p][l] : 0.0;
+            utc[p][l] = 2.0 * c;
+            ucur[p][l] = 1.0;
+            uprev[p][l] = c;  // c_{-1} = c_1: the first advance yields c_1 exactly
+            uacc[p][l] = 0.0;
         }
-        const double cl = c1[p][D - 1], tl = 2.0 * cl;
+        const double cs = D >= 2 ? c1[p][D >= 2 ? D - 2 : 0] : 1.0;
+        t2c[p] = 2.0 * cs;
+        t2[p][0] = 1.0;
+        t2[p][1] = cs;
+#pragma unroll
+        for (int s = 2; s < S2; ++s) t2[p][s] = fma(t2c[p], t2[p][s - 1], -t2[p][s - 2]);
+        const double cl = c1[p][D - 1];
+        tl[p] = 2.0 * cl;
         leaf[p][0] = 1.0;
         leaf[p][1] = cl;
 #pragma unroll
-        for (int b = 2; b < LT; ++b) leaf[p][b] = fma(tl, leaf[p][b - 1], -leaf[p][b - 2]);
-        y[p] = 0.0;
+        for (int b = 2; b < LT; ++b) leaf[p][b] = fma(tl[p], leaf[p][b - 1], -leaf[p][b - 2]);
+        acc2[p] = 0.0;
+        g2p[p] = t2[p][S2 - 2];
+        g2c[p] = t2[p][S2 - 1];
     }
 
     load_tile(sm, 0, st, row, 0);
@@ -92,102 +152,94 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, const SeriesTiles& 
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int n_runs = st.tiles[t].y;
+        const int n_words = st.tiles[t].y;
         const uint32_t* pw = sm.prog[buf];
         const double2* pa = reinterpret_cast<const double2*>(sm.alpha[buf]);
-        for (int n = 0; n < n_runs; ++n) {
-            const uint32_t w = pw[n];
-            const int L = static_cast<int>(w & 15u);
-            const int R = static_cast<int>(w >> 4);
-            if constexpr (D >= 2) {
-                if (L == D - 2) {
-                    // sibling run: advance the deepest internal level
+        int wi = 0;
+        while (wi < n_words) {
+            const uint32_t h = pw[wi];
+            const int L = static_cast<int>(h & 15u);
+            const int n = static_cast<int>((h >> 4) & 0x3FFFu);
+            const int s0 = static_cast<int>(h >> 18);
+            const uint32_t* runs = pw + wi + 1;
+            wi += 1 + n;
+            if (L != kContGroup) {
+                if (L != kFirstGroup) {
+                    // close the finished group and the upper nodes above it, advance level L
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
-                        const double nx = fma(tc[p][D - 2], cur[p][D - 2], -prev[p][D - 2]);
-                        prev[p][D - 2] = cur[p][D - 2];
-                        cur[p][D - 2] = nx;
-                    }
-                } else if (L != kFirstRun) {
+                        if constexpr (D > 2) {
+                            uacc[p][D - 3] = fma(ucur[p][D - 3], acc2[p], uacc[p][D - 3]);
 #pragma unroll
-                    for (int p = 0; p < P; ++p) {
+                            for (int l = D - 4; l >= 0; --l) {
+                                if (l >= L) {
+                                    uacc[p][l] = fma(ucur[p][l], uacc[p][l + 1], uacc[p][l]);
+                                    uacc[p][l + 1] = 0.0;
+                                }
+                            }
 #pragma unroll
-                        for (int l = D - 3; l >= 0; --l) {
-                            if (l >= L) {
-                                acc[p][l] = fma(cur[p][l], acc[p][l + 1], acc[p][l]);
-                                acc[p][l + 1] = 0.0;
+                            for (int l = 0; l < D - 2; ++l) {
+                                if (l == L) {
+                                    const double nx = fma(utc[p][l], ucur[p][l], -uprev[p][l]);
+                                    uprev[p][l] = ucur[p][l];
+                                    ucur[p][l] = nx;
+                                } else if (l > L) {
+                                    ucur[p][l] = 1.0;
+                                    uprev[p][l] = 0.5 * utc[p][l];
+                                }
                             }
                         }
-#pragma unroll
-                        for (int l = 0; l < D - 1; ++l) {
-                            if (l == L) {
-                                const double nx = fma(tc[p][l], cur[p][l], -prev[p][l]);
-                                prev[p][l] = cur[p][l];
-                                cur[p][l] = nx;
-                            } else if (l > L) {
-                                cur[p][l] = 1.0;
-                                prev[p][l] = 0.5 * tc[p][l];
-                            }
-                        }
+                        acc2[p] = 0.0;
                     }
                 }
-            }
-            // leaf run: z = sum_{b<R} alpha'[b] c_b
-            double z0[P], z1[P];
-#pragma unroll
-            for (int p = 0; p < P; ++p) z0[p] = z1[p] = 0.0;
-#pragma unroll
-            for (int b2 = 0; b2 < LT / 2; ++b2) {
-                if (2 * b2 < R) {
-                    const double2 a = pa[b2];
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        z0[p] = fma(a.x, leaf[p][2 * b2], z0[p]);
-                        z1[p] = fma(a.y, leaf[p][2 * b2 + 1], z1[p]);
-                    }
-                }
-            }
-            if (R > LT) {
-                // long run: continue the Chebyshev recurrence from (c_{LT-2}, c_{LT-1})
-                double cp[P], cc[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
-                    cp[p] = leaf[p][LT - 2];
-                    cc[p] = leaf[p][LT - 1];
-                }
-                const int pairs = (R + 1) >> 1;
-                for (int b2 = LT / 2; b2 < pairs; ++b2) {
-                    const double2 a = pa[b2];
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        const double tl = 2.0 * leaf[p][1];
-                        const double e = fma(tl, cc[p], -cp[p]);  // c_{2 b2}
-                        const double o = fma(tl, e, -cc[p]);      // c_{2 b2 + 1}
-                        z0[p] = fma(a.x, e, z0[p]);
-                        z1[p] = fma(a.y, o, z1[p]);
-                        cp[p] = e;
-                        cc[p] = o;
-                    }
+                    g2p[p] = t2[p][S2 - 2];
+                    g2c[p] = t2[p][S2 - 1];
                 }
             }
-            pa += (R + 1) >> 1;
+            int s = 0;
+            if (s0 == 0) {
+                // siblings inside the register table: static indices
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const double z = z0[p] + z1[p];
-                if constexpr (D >= 2)
-                    acc[p][D - 2] = fma(cur[p][D - 2], z, acc[p][D - 2]);
-                else
-                    y[p] += z;
+                for (int ss = 0; ss < S2; ++ss) {
+                    if (ss < n) {
+                        double z0[P], z1[P];
+                        leaf_run<P, LT>(pa, static_cast<int>(runs[ss]), leaf, tl, z0, z1);
+#pragma unroll
+                        for (int p = 0; p < P; ++p) {
+                            acc2[p] = fma(t2[p][ss], z0[p], acc2[p]);
+                            acc2[p] = fma(t2[p][ss], z1[p], acc2[p]);
+                        }
+                    }
+                }
+                s = S2;
+            }
+            // siblings past the table (relative index ss, absolute s0 + ss >= S2):
+            // advance the recurrence (g2p, g2c) = (c_{s-2}, c_{s-1})
+            for (int ss = s; ss < n; ++ss) {
+                double z0[P], z1[P];
+                leaf_run<P, LT>(pa, static_cast<int>(runs[ss]), leaf, tl, z0, z1);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double cs = fma(t2c[p], g2c[p], -g2p[p]);
+                    g2p[p] = g2c[p];
+                    g2c[p] = cs;
+                    acc2[p] = fma(cs, z0[p] + z1[p], acc2[p]);
+                }
             }
         }
         __syncthreads();  // the buffer is refilled by the next iteration's prefetch
     }
-    if constexpr (D >= 2) {
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
+    for (int p = 0; p < P; ++p) {
+        if constexpr (D > 2) {
+            uacc[p][D - 3] = fma(ucur[p][D - 3], acc2[p], uacc[p][D - 3]);
 #pragma unroll
-            for (int l = D - 3; l >= 0; --l) acc[p][l] = fma(cur[p][l], acc[p][l + 1], acc[p][l]);
-            y[p] = acc[p][0];
+            for (int l = D - 4; l >= 0; --l) uacc[p][l] = fma(ucur[p][l], uacc[p][l + 1], uacc[p][l]);
+            y[p] = uacc[p][0];
+        } else {
+            y[p] = acc2[p];
         }
     }
 }
