@@ -188,7 +188,7 @@ struct Program {
 
 constexpr int kHostTileA = 2048;  // == kTileA in series_block.cuh
 constexpr int kHostTileP = 1024;  // == kTileP
-constexpr uint32_t kFirstGroupCode = 15, kContGroupCode = 14;
+constexpr uint32_t kFirstGroupCode = 15;
 
 // Group program of series_block.cuh: one group per upper prefix (k_0..k_{D-3}),
 // holding the leaf-run lengths of its siblings k_{D-2} = 0..n-1, cut into
@@ -199,7 +199,6 @@ Program build_program(const Gamma& g) {
     Program p;
     const int d = g.dim;
     const int64_t K = g.size();
-    const int S2 = k1_s2(d);
     p.pack_pos.resize(static_cast<size_t>(K));
     p.pack_scale.resize(static_cast<size_t>(K));
     auto at = [&](int64_t i, int l) { return g.rows[static_cast<size_t>(i * d + l)]; };
@@ -264,45 +263,36 @@ Program build_program(const Gamma& g) {
         r = e;
     }
 
-    // 3. tiles: a group chunk never splits a run; the first chunk of a group holds
-    // at least its first min(n, S2) siblings (the register-table part)
+    // 3. tiles of whole runs: one 64-bit word per run (series_block.cuh), each
+    // tile's words followed by a zero word for the pipelined prefetch
     int4 cur = make_int4(0, 0, 0, 0);
     int64_t alpha_pos = 0;
     auto close = [&] {
         if (cur.y == 0) return;
         p.tiles.push_back(cur);
+        p.tile_prog.push_back(0);
+        p.tile_prog.push_back(0);
         while (p.tile_prog.size() % 4) p.tile_prog.push_back(0);
     };
     auto open = [&] { cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0); };
-    auto padded = [&](size_t r) { return (runs[r].R + 1) & ~int64_t{1}; };
     open();
     for (const Group& gr : groups) {
-        size_t s = 0;
-        while (s < gr.n) {
-            // the minimum this chunk must hold
-            const size_t need = s == 0 ? std::min<size_t>(gr.n, static_cast<size_t>(S2)) : 1;
-            int64_t need_a = 0;
-            for (size_t q = 0; q < need; ++q) need_a += padded(gr.r0 + s + q);
-            if (need_a > kHostTileA || static_cast<int64_t>(need) + 1 > kHostTileP)
-                fail(QRMC_ENOTIMPL, "a sibling group exceeds a shared-memory tile");
-            if (cur.w + need_a > kHostTileA || cur.y + static_cast<int64_t>(need) + 1 > kHostTileP) {
+        for (size_t s = 0; s < gr.n; ++s) {
+            const int64_t R = runs[gr.r0 + s].R;
+            const int64_t pad = (R + 1) & ~int64_t{1};
+            if (pad > kHostTileA || R >= 4096 || s >= 4096)
+                fail(QRMC_ENOTIMPL, fmt("leaf run of %lld coefficients exceeds a shared-memory tile", (long long)R));
+            if (cur.w + pad > kHostTileA || cur.y + 1 > kHostTileP) {
                 close();
                 open();
             }
-            size_t take = need;
-            int64_t take_a = need_a;
-            while (s + take < gr.n && cur.w + take_a + padded(gr.r0 + s + take) <= kHostTileA &&
-                   cur.y + static_cast<int64_t>(take) + 2 <= kHostTileP) {
-                take_a += padded(gr.r0 + s + take);
-                ++take;
-            }
-            const uint32_t L = s == 0 ? gr.L : kContGroupCode;
-            p.tile_prog.push_back(L | (static_cast<uint32_t>(take) << 4) | (static_cast<uint32_t>(s) << 18));
-            for (size_t q = 0; q < take; ++q) p.tile_prog.push_back(static_cast<uint32_t>(runs[gr.r0 + s + q].R));
-            cur.y += static_cast<int>(take) + 1;
-            cur.w += static_cast<int>(take_a);
-            alpha_pos += take_a;
-            s += take;
+            const uint32_t x = static_cast<uint32_t>(cur.w / 2) | (static_cast<uint32_t>(R) << 11);
+            const uint32_t y = static_cast<uint32_t>(s) | (s == 0 ? (1u << 12) | (gr.L << 13) : 0u);
+            p.tile_prog.push_back(x);
+            p.tile_prog.push_back(y);
+            cur.y += 1;
+            cur.w += static_cast<int>(pad);
+            alpha_pos += pad;
         }
     }
     close();
@@ -657,6 +647,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     pa.basis_size = P->K;
 
     cuda_check(configure_project(d, project_smem_bytes(pa)), "k_project attributes");
+    cuda_check(configure_series_kernels(), "series kernel attributes");
     P->ev.resize(3 * static_cast<size_t>(cfg.steps) + 1);
     for (auto& e : P->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     P->launches_per_run = 3 * cfg.steps;
@@ -728,7 +719,10 @@ void download(qrmc_gpu_plan& P, double* coeffs, size_t len) {
 // A throwaway single-GPU context for the probe entry points.
 struct Scratch {
     std::unique_ptr<qrmc_gpu_session, void (*)(qrmc_gpu_session*)> s{nullptr, destroy_session};
-    Scratch() { s.reset(make_session(current_device(), 0, 1, nullptr).release()); }
+    Scratch() {
+        s.reset(make_session(current_device(), 0, 1, nullptr).release());
+        cuda_check(configure_series_kernels(), "series kernel attributes");
+    }
 };
 
 // Minimal StepArgs for probes that only need the problem and measure.

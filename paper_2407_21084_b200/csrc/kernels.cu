@@ -48,10 +48,19 @@ __device__ __forceinline__ void sample_start(const MeasureDev& m, int d, Stream&
 // per dimension: k1_p / k1_s2 / k1_lt (qrmc_types.h).
 constexpr int kK1Threads = 128;
 
+// dynamic shared memory of a series kernel: coefficient/program tiles + the
+// per-thread sibling table c_{D-2}[0..S2) for P points
+template <int D>
+constexpr size_t series_smem_bytes(int P) {
+    return sizeof(SeriesSmem) + static_cast<size_t>(k1_s2(D)) * P * kK1Threads * sizeof(double);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
     constexpr int P = k1_p(D), S2 = k1_s2(D), LT = k1_lt(D);
-    __shared__ SeriesSmem sm;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    SeriesSmem& sm = *reinterpret_cast<SeriesSmem*>(dsm);
+    double* t2s = reinterpret_cast<double*>(dsm + sizeof(SeriesSmem));
     __shared__ int s_abort;
     if (threadIdx.x == 0) s_abort = *a.abort_flag;
     __syncthreads();
@@ -99,7 +108,7 @@ __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
 #pragma unroll
                 for (int l = 0; l < D; ++l)
                     c1[p][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xn[p][l], l)));
-            series_block<D, P, S2, LT>(sm, a.tiles, a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp, c1, ys);
+            series_block<D, P, S2, LT>(sm, t2s, a.tiles, a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp, c1, ys);
 #pragma unroll
             for (int p = 0; p < P; ++p) y[p] = DMUL(ys[p], damping_weight<D>(xn[p], a.q));
         }
@@ -294,7 +303,9 @@ template <int D>
 __global__ void __launch_bounds__(kK1Threads) k_eval_points(const StepArgs a, const double* alpha_row,
                                                             const double* x, int64_t n, double q,
                                                             int with_weight, double* out) {
-    __shared__ SeriesSmem sm;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    SeriesSmem& sm = *reinterpret_cast<SeriesSmem*>(dsm);
+    double* t2s = reinterpret_cast<double*>(dsm + sizeof(SeriesSmem));
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t rr = r < n ? r : n - 1;
     double p[D], c1[1][D], y[1];
@@ -303,7 +314,7 @@ __global__ void __launch_bounds__(kK1Threads) k_eval_points(const StepArgs a, co
         p[l] = x[rr * D + l];
         c1[0][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, p[l], l)));
     }
-    series_block<D, 1, k1_s2(D), k1_lt(D)>(sm, a.tiles, alpha_row, c1, y);
+    series_block<D, 1, k1_s2(D), k1_lt(D)>(sm, t2s, a.tiles, alpha_row, c1, y);
     if (r < n) out[r] = with_weight ? DMUL(y[0], damping_weight<D>(p, q)) : y[0];
 }
 
@@ -313,7 +324,9 @@ template <int D>
 __global__ void __launch_bounds__(kK1Threads) k_mse(const StepArgs a, double kappa, double lam, double horizon,
                                                     uint64_t eval_seed, int eval_points, double* sq,
                                                     double* sq_u) {
-    __shared__ SeriesSmem sm;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    SeriesSmem& sm = *reinterpret_cast<SeriesSmem*>(dsm);
+    double* t2s = reinterpret_cast<double*>(dsm + sizeof(SeriesSmem));
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t r = r0 < eval_points ? r0 : eval_points - 1;
     const int i = blockIdx.y;
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(kK1Threads) k_mse(const StepArgs a, double kap
         c1[0][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, p[l], l)));
     }
     const double w = damping_weight<D>(p, a.q);
-    series_block<D, 1, k1_s2(D), k1_lt(D)>(sm, a.tiles, a.alpha_packed + static_cast<int64_t>(i) * a.kp, c1, y);
+    series_block<D, 1, k1_s2(D), k1_lt(D)>(sm, t2s, a.tiles, a.alpha_packed + static_cast<int64_t>(i) * a.kp, c1, y);
     if (r0 >= eval_points) return;
     const double approx = y[0];
     const double t = DMUL(static_cast<double>(i), a.dt);
@@ -350,12 +363,32 @@ __global__ void __launch_bounds__(kK1Threads) k_mse(const StepArgs a, double kap
         default: return cudaErrorInvalidValue;      \
     }
 
+// Opt every series kernel into > 48 KiB of dynamic shared memory (once per process).
+cudaError_t configure_series_kernels() {
+    static cudaError_t status = [] {
+        cudaError_t e = cudaSuccess;
+        auto set = [&](const void* f, size_t bytes) {
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+        };
+#define QRMC_CONFIGURE(Dv)                                                                           \
+    set(reinterpret_cast<const void*>(&k_responses<Dv>), series_smem_bytes<Dv>(k1_p(Dv)));          \
+    set(reinterpret_cast<const void*>(&k_eval_points<Dv>), series_smem_bytes<Dv>(1));              \
+    set(reinterpret_cast<const void*>(&k_mse<Dv>), series_smem_bytes<Dv>(1));
+        QRMC_CONFIGURE(1) QRMC_CONFIGURE(2) QRMC_CONFIGURE(3) QRMC_CONFIGURE(4)
+        QRMC_CONFIGURE(5) QRMC_CONFIGURE(6) QRMC_CONFIGURE(7) QRMC_CONFIGURE(8)
+#undef QRMC_CONFIGURE
+        return e;
+    }();
+    return status;
+}
+
 cudaError_t launch_responses(const StepArgs& a, cudaStream_t st) {
     if (a.n_owned == 0) return cudaSuccess;
     QRMC_DISPATCH_D(a.prob.dim, {
         const int64_t per_cta = static_cast<int64_t>(kK1Threads) * k1_p(D);
         const unsigned blocks = static_cast<unsigned>((a.n_owned + per_cta - 1) / per_cta);
-        k_responses<D><<<blocks, kK1Threads, 0, st>>>(a);
+        k_responses<D><<<blocks, kK1Threads, series_smem_bytes<D>(k1_p(D)), st>>>(a);
     });
     return cudaGetLastError();
 }
@@ -412,14 +445,14 @@ cudaError_t launch_cloud_paths(const StepArgs& a, int64_t first, int64_t n, doub
 cudaError_t launch_eval_points(const StepArgs& a, const double* alpha_row, const double* x, int64_t n,
                                double q, int with_weight, double* out, cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>((n + 127) / 128);
-    QRMC_DISPATCH_D(a.prob.dim, (k_eval_points<D><<<blocks, 128, 0, st>>>(a, alpha_row, x, n, q, with_weight, out)));
+    QRMC_DISPATCH_D(a.prob.dim, (k_eval_points<D><<<blocks, kK1Threads, series_smem_bytes<D>(1), st>>>(a, alpha_row, x, n, q, with_weight, out)));
     return cudaGetLastError();
 }
 
 cudaError_t launch_mse(const StepArgs& a, double kappa, double lam, double horizon, uint64_t eval_seed,
                        int eval_points, double* sq, double* sq_u, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((eval_points + 127) / 128), static_cast<unsigned>(a.steps));
-    QRMC_DISPATCH_D(a.prob.dim, (k_mse<D><<<grid, 128, 0, st>>>(a, kappa, lam, horizon, eval_seed, eval_points, sq, sq_u)));
+    QRMC_DISPATCH_D(a.prob.dim, (k_mse<D><<<grid, kK1Threads, series_smem_bytes<D>(1), st>>>(a, kappa, lam, horizon, eval_seed, eval_points, sq, sq_u)));
     return cudaGetLastError();
 }
 

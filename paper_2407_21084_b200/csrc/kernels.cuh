@@ -61,6 +61,7 @@ struct FinishArgs {
     const double* pack_scale;    // sqrt2^{nnz(k)}
 };
 
+cudaError_t configure_series_kernels();  // once per process, before the first series launch
 cudaError_t launch_responses(const StepArgs& a, cudaStream_t st);
 size_t project_smem_bytes(const ProjArgs& p);
 cudaError_t configure_project(int dim, size_t smem);

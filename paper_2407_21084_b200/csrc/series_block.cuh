@@ -5,26 +5,25 @@
 // Sum factorisation over Gamma's lexicographic trie. With c_l[v] = cos(v pi u_l)
 // and alpha'_k = alpha_k sqrt2^{nnz(k)} (packed by host.cpp):
 //     y = sum_{upper prefix} (prod_{l<D-2} c_l) sum_s c_{D-2}[s] sum_b alpha'[.., s, b] c_{D-1}[b]
-// The two deepest levels are evaluated from per-point REGISTER tables,
-// c_{D-2}[0..S2) and c_{D-1}[0..LT), computed once per evaluation, so every
-// term inside the tables costs exactly one FMA and every leaf run one more
-// (its fold into the sibling sum). Indices beyond the tables continue the
-// reference's three-term Chebyshev recurrence (cosine_basis.cpp:79-86) in
-// registers. Levels above D-2 ("upper" levels) change rarely and carry
-// (2c1, c_prev, c_cur, acc) recurrence state.
+// Leaf values c_{D-1}[0..LT) live in a per-point REGISTER table (static
+// indices inside a Duff's-device jump table, so a run of R coefficients costs
+// exactly R FMAs), sibling weights c_{D-2}[0..S2) in a per-thread SHARED
+// table (one LDS per run), both computed once per evaluation with the
+// reference's three-term recurrence (cosine_basis.cpp:79-86); indices past
+// the tables continue that recurrence in registers. Levels above D-2 change
+// rarely and carry (2c1, c_prev, c_cur, acc) recurrence state.
 //
-// Program (host.cpp build_program): one GROUP per upper prefix (k_0..k_{D-3}),
-//   word 0: bits 0..3  transition level L of the upper prefix vs the previous
-//                      group (kFirstGroup for the first, kContGroup when the
-//                      group continues from the previous tile),
-//           bits 4..17 number of sibling runs n in this chunk,
-//           bits 18..31 first sibling index s0 (0, or >= S2 for continuations)
-//   words 1..n: leaf run lengths R_s (leaf indices 0..R_s-1)
-// and the packed coefficients of each run, padded to even length. Groups are
-// cut into tiles (<= kTileA coefficients, <= kTileP words) that stream
-// through shared memory with cp.async double buffering; inner loops read
-// coefficients as 16-byte shared-memory broadcasts. Control flow is uniform
-// across the CTA (every thread walks the same program), so it never diverges.
+// Program (host.cpp build_program): one 64-bit word per leaf run,
+//   x: bits 0..10  pair offset of the run's coefficients inside the tile
+//      bits 11..22 run length R
+//   y: bits 0..11  sibling index s = k_{D-2}
+//      bit  12     first run of a group (upper prefix k_0..k_{D-3} changed)
+//      bits 13..16 transition level L of that prefix change (15: first group)
+// cut into tiles of <= kTileA coefficients / <= kTileP runs that stream
+// through shared memory with cp.async double buffering. The node loop is
+// software-pipelined: the next run's word and first coefficient pair are
+// loaded while the current run computes. Control flow is uniform across the
+// CTA (every thread walks the same program), so it never diverges.
 #pragma once
 
 #include <cstdint>
@@ -34,13 +33,12 @@
 namespace qrmc_dev {
 
 constexpr int kTileA = 2048;    // coefficients per shared-memory tile (16 KiB)
-constexpr int kTileP = 1024;    // program words per tile (4 KiB)
+constexpr int kTileP = 1024;    // runs per tile (8 KiB of words)
 constexpr int kFirstGroup = 15; // transition code of the first group
-constexpr int kContGroup = 14;  // continuation of the previous tile's group
 
 struct SeriesSmem {
-    double alpha[2][kTileA];
-    uint32_t prog[2][kTileP];
+    double alpha[2][kTileA + 4];  // +4: the pipelined prefetch may read one pair past the tile
+    uint2 prog[2][kTileP + 2];    // + a zero word after the last run (pipelined prefetch)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -57,62 +55,22 @@ __device__ __forceinline__ void load_tile(SeriesSmem& sm, int buf, const SeriesT
     const int na = d.w >> 1;  // 16-byte chunks of coefficients
     const double* ga = row + d.z;
     for (int c = threadIdx.x; c < na; c += blockDim.x) cp_async16(&sm.alpha[buf][2 * c], ga + 2 * c);
-    const int np = (d.y + 3) >> 2;
+    const int np = (d.y + 2) >> 1;  // two 8-byte words per chunk, incl. the zero pad word
     const uint32_t* gp = st.prog + d.x;
-    for (int c = threadIdx.x; c < np; c += blockDim.x) cp_async16(&sm.prog[buf][4 * c], gp + 4 * c);
-}
-
-// Leaf run z = sum_{b<R} alpha'[b] c_b for P points; pa advances past the run.
-template <int P, int LT>
-__device__ __forceinline__ void leaf_run(const double2*& pa, int R, const double (&leaf)[P][LT],
-                                         const double (&tl)[P], double (&z0)[P], double (&z1)[P]) {
-#pragma unroll
-    for (int p = 0; p < P; ++p) z0[p] = z1[p] = 0.0;
-#pragma unroll
-    for (int b2 = 0; b2 < LT / 2; ++b2) {
-        if (2 * b2 < R) {
-            const double2 a = pa[b2];
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                z0[p] = fma(a.x, leaf[p][2 * b2], z0[p]);
-                z1[p] = fma(a.y, leaf[p][2 * b2 + 1], z1[p]);
-            }
-        }
-    }
-    if (R > LT) {
-        double cp[P], cc[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-            cp[p] = leaf[p][LT - 2];
-            cc[p] = leaf[p][LT - 1];
-        }
-        const int pairs = (R + 1) >> 1;
-        for (int b2 = LT / 2; b2 < pairs; ++b2) {
-            const double2 a = pa[b2];
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const double e = fma(tl[p], cc[p], -cp[p]);  // c_{2 b2}
-                const double o = fma(tl[p], e, -cc[p]);      // c_{2 b2 + 1}
-                z0[p] = fma(a.x, e, z0[p]);
-                z1[p] = fma(a.y, o, z1[p]);
-                cp[p] = e;
-                cc[p] = o;
-            }
-        }
-    }
-    pa += (R + 1) >> 1;
+    for (int c = threadIdx.x; c < np; c += blockDim.x) cp_async16(&sm.prog[buf][2 * c], gp + 4 * c);
 }
 
 // Evaluate the series of coefficient row `row` at P points per thread.
-// c1[p][l] = cos(pi u_l) of point p. Must be called by every thread of the CTA.
+// c1[p][l] = cos(pi u_l) of point p; t2s: shared scratch of S2*P*blockDim doubles.
+// Must be called by every thread of the CTA.
 template <int D, int P, int S2, int LT>
-__device__ __forceinline__ void series_block(SeriesSmem& sm, const SeriesTiles& st, const double* row,
-                                             const double (&c1)[P][D], double (&y)[P]) {
-    static_assert(LT % 2 == 0 && LT >= 2 && S2 >= 2, "table sizes");
+__device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const SeriesTiles& st,
+                                             const double* row, const double (&c1)[P][D], double (&y)[P]) {
+    static_assert(LT % 2 == 0 && LT >= 4 && LT <= 32 && S2 >= 2, "table sizes");
     constexpr int NU = D > 2 ? D - 2 : 1;  // upper levels 0..D-3
+    const int tid = threadIdx.x, nt = blockDim.x;
     double utc[P][NU], ucur[P][NU], uprev[P][NU], uacc[P][NU];
-    double t2[P][S2], leaf[P][LT], tl[P], t2c[P];
-    double acc2[P], g2p[P], g2c[P];  // sibling sum of the current group; recurrence past S2
+    double leaf[P][LT], tl[P], t2c[P], acc2[P], g2p[P], g2c[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
 #pragma unroll
@@ -123,23 +81,29 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, const SeriesTiles& 
             uprev[p][l] = c;  // c_{-1} = c_1: the first advance yields c_1 exactly
             uacc[p][l] = 0.0;
         }
+        // sibling table c_{D-2}[0..S2) -> shared memory, layout [s][p][tid]
         const double cs = D >= 2 ? c1[p][D >= 2 ? D - 2 : 0] : 1.0;
         t2c[p] = 2.0 * cs;
-        t2[p][0] = 1.0;
-        t2[p][1] = cs;
+        double a = 1.0, b = cs;
+        t2s[(0 * P + p) * nt + tid] = a;
+        t2s[(1 * P + p) * nt + tid] = b;
 #pragma unroll
-        for (int s = 2; s < S2; ++s) t2[p][s] = fma(t2c[p], t2[p][s - 1], -t2[p][s - 2]);
+        for (int s = 2; s < S2; ++s) {
+            const double c = fma(t2c[p], b, -a);
+            t2s[(s * P + p) * nt + tid] = c;
+            a = b;
+            b = c;
+        }
+        g2p[p] = a;  // (c_{S2-2}, c_{S2-1}): start of the recurrence past the table
+        g2c[p] = b;
         const double cl = c1[p][D - 1];
         tl[p] = 2.0 * cl;
         leaf[p][0] = 1.0;
         leaf[p][1] = cl;
 #pragma unroll
-        for (int b = 2; b < LT; ++b) leaf[p][b] = fma(tl[p], leaf[p][b - 1], -leaf[p][b - 2]);
+        for (int k = 2; k < LT; ++k) leaf[p][k] = fma(tl[p], leaf[p][k - 1], -leaf[p][k - 2]);
         acc2[p] = 0.0;
-        g2p[p] = t2[p][S2 - 2];
-        g2c[p] = t2[p][S2 - 1];
     }
-
     load_tile(sm, 0, st, row, 0);
     cp_async_commit();
     for (int t = 0; t < st.n_tiles; ++t) {
@@ -152,23 +116,26 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, const SeriesTiles& 
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int n_words = st.tiles[t].y;
-        const uint32_t* pw = sm.prog[buf];
+        const int n_runs = st.tiles[t].y;
+        const uint2* pw = sm.prog[buf];
         const double2* pa = reinterpret_cast<const double2*>(sm.alpha[buf]);
-        int wi = 0;
-        while (wi < n_words) {
-            const uint32_t h = pw[wi];
-            const int L = static_cast<int>(h & 15u);
-            const int n = static_cast<int>((h >> 4) & 0x3FFFu);
-            const int s0 = static_cast<int>(h >> 18);
-            const uint32_t* runs = pw + wi + 1;
-            wi += 1 + n;
-            if (L != kContGroup) {
-                if (L != kFirstGroup) {
-                    // close the finished group and the upper nodes above it, advance level L
+        uint2 w = pw[0];  // pair offsets are < 1024 (masked 0x3FF)
+        double2 a0 = pa[w.x & 0x3FFu];
+        for (int n = 0; n < n_runs; ++n) {
+            // software pipeline: next word and its first pair
+            const uint2 wn = pw[n + 1];
+            const double2 a0n = pa[wn.x & 0x3FFu];
+            const int off = static_cast<int>(w.x & 0x3FFu);
+            const int R = static_cast<int>((w.x >> 11) & 0xFFFu);
+            const int s = static_cast<int>(w.y & 0xFFFu);
+            if (w.y & 0x1000u) {
+                // first run of a group: close the previous group and the upper nodes
+                // above it, advance level L of the upper prefix
+                const int L = static_cast<int>((w.y >> 13) & 15u);
+                if constexpr (D > 2) {
+                    if (L != kFirstGroup) {
 #pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        if constexpr (D > 2) {
+                        for (int p = 0; p < P; ++p) {
                             uacc[p][D - 3] = fma(ucur[p][D - 3], acc2[p], uacc[p][D - 3]);
 #pragma unroll
                             for (int l = D - 4; l >= 0; --l) {
@@ -189,45 +156,86 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, const SeriesTiles& 
                                 }
                             }
                         }
-                        acc2[p] = 0.0;
                     }
                 }
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
-                    g2p[p] = t2[p][S2 - 2];
-                    g2c[p] = t2[p][S2 - 1];
+                    acc2[p] = 0.0;
+                    g2p[p] = t2s[((S2 - 2) * P + p) * nt + tid];
+                    g2c[p] = t2s[((S2 - 1) * P + p) * nt + tid];
                 }
             }
-            int s = 0;
-            if (s0 == 0) {
-                // siblings inside the register table: static indices
+            // sibling weight c_{D-2}[s]
+            double ts[P];
+            if (s < S2) {
 #pragma unroll
-                for (int ss = 0; ss < S2; ++ss) {
-                    if (ss < n) {
-                        double z0[P], z1[P];
-                        leaf_run<P, LT>(pa, static_cast<int>(runs[ss]), leaf, tl, z0, z1);
-#pragma unroll
-                        for (int p = 0; p < P; ++p) {
-                            acc2[p] = fma(t2[p][ss], z0[p], acc2[p]);
-                            acc2[p] = fma(t2[p][ss], z1[p], acc2[p]);
-                        }
-                    }
-                }
-                s = S2;
-            }
-            // siblings past the table (relative index ss, absolute s0 + ss >= S2):
-            // advance the recurrence (g2p, g2c) = (c_{s-2}, c_{s-1})
-            for (int ss = s; ss < n; ++ss) {
-                double z0[P], z1[P];
-                leaf_run<P, LT>(pa, static_cast<int>(runs[ss]), leaf, tl, z0, z1);
+                for (int p = 0; p < P; ++p) ts[p] = t2s[(s * P + p) * nt + tid];
+            } else {
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
-                    const double cs = fma(t2c[p], g2c[p], -g2p[p]);
+                    const double c = fma(t2c[p], g2c[p], -g2p[p]);
                     g2p[p] = g2c[p];
-                    g2c[p] = cs;
-                    acc2[p] = fma(cs, z0[p] + z1[p], acc2[p]);
+                    g2c[p] = c;
+                    ts[p] = c;
                 }
             }
+            // leaf run z = sum_{b<R} alpha'[b] c_b: Duff's device over pairs, a jump
+            // table executes exactly the run's pairs
+            const double2* ra = pa + off;
+            double z0[P], z1[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                z0[p] = a0.x * leaf[p][0];
+                z1[p] = a0.y * leaf[p][1];
+            }
+            const int np = min((R + 1) >> 1, LT / 2);
+#define QRMC_LEAF_PAIR(i)                                          \
+    case (i) + 1:                                                  \
+        if constexpr ((i) < LT / 2 && (i) > 0) {                   \
+            const double2 aa = ra[(i)];                            \
+            _Pragma("unroll") for (int p = 0; p < P; ++p) {        \
+                z0[p] = fma(aa.x, leaf[p][2 * (i)], z0[p]);        \
+                z1[p] = fma(aa.y, leaf[p][2 * (i) + 1], z1[p]);    \
+            }                                                      \
+        }                                                          \
+        [[fallthrough]];
+            switch (np) {
+                QRMC_LEAF_PAIR(15) QRMC_LEAF_PAIR(14) QRMC_LEAF_PAIR(13) QRMC_LEAF_PAIR(12)
+                QRMC_LEAF_PAIR(11) QRMC_LEAF_PAIR(10) QRMC_LEAF_PAIR(9) QRMC_LEAF_PAIR(8)
+                QRMC_LEAF_PAIR(7) QRMC_LEAF_PAIR(6) QRMC_LEAF_PAIR(5) QRMC_LEAF_PAIR(4)
+                QRMC_LEAF_PAIR(3) QRMC_LEAF_PAIR(2) QRMC_LEAF_PAIR(1)
+                default: break;
+            }
+#undef QRMC_LEAF_PAIR
+            if (R > LT) {
+                // long run: continue the Chebyshev recurrence from (c_{LT-2}, c_{LT-1})
+                double cp[P], cc[P];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    cp[p] = leaf[p][LT - 2];
+                    cc[p] = leaf[p][LT - 1];
+                }
+                const int pairs = (R + 1) >> 1;
+                for (int b2 = LT / 2; b2 < pairs; ++b2) {
+                    const double2 aa = ra[b2];
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const double e = fma(tl[p], cc[p], -cp[p]);  // c_{2 b2}
+                        const double o = fma(tl[p], e, -cc[p]);      // c_{2 b2 + 1}
+                        z0[p] = fma(aa.x, e, z0[p]);
+                        z1[p] = fma(aa.y, o, z1[p]);
+                        cp[p] = e;
+                        cc[p] = o;
+                    }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                acc2[p] = fma(ts[p], z0[p], acc2[p]);
+                acc2[p] = fma(ts[p], z1[p], acc2[p]);
+            }
+            w = wn;
+            a0 = a0n;
         }
         __syncthreads();  // the buffer is refilled by the next iteration's prefetch
     }
