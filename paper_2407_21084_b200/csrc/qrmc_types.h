@@ -12,7 +12,7 @@ constexpr int kMaxDim = 8;
 
 // Series-kernel shape per dimension D (series_block.cuh): paths per thread P,
 // register-table sizes S2 (level D-2) and LT (leaf level D-1).
-constexpr int k1_p(int d) { return d == 2 || d >= 7 ? 1 : 2; }
+constexpr int k1_p(int d) { return d <= 2 || d >= 7 ? 1 : 2; }
 constexpr int k1_s2(int d) { return d <= 1 ? 2 : d == 2 ? 32 : d == 3 ? 16 : 8; }
 constexpr int k1_lt(int d) { return d <= 2 ? 32 : d <= 4 ? 16 : 8; }
 

@@ -29,6 +29,7 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "leaf_chain.cuh"
 
 namespace qrmc_dev {
 
@@ -37,7 +38,7 @@ constexpr int kTileP = 1024;    // runs per tile (8 KiB of words)
 constexpr int kFirstGroup = 15; // transition code of the first group
 
 struct SeriesSmem {
-    double alpha[2][kTileA + 4];  // +4: the pipelined prefetch may read one pair past the tile
+    double alpha[2][kTileA + 8];  // +8: the leaf chain preloads 4 pairs, possibly past a tile's end
     uint2 prog[2][kTileP + 2];    // + a zero word after the last run (pipelined prefetch)
 };
 
@@ -120,11 +121,9 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
         const uint2* pw = sm.prog[buf];
         const double2* pa = reinterpret_cast<const double2*>(sm.alpha[buf]);
         uint2 w = pw[0];  // pair offsets are < 1024 (masked 0x3FF)
-        double2 a0 = pa[w.x & 0x3FFu];
+        const unsigned pa_s = static_cast<unsigned>(__cvta_generic_to_shared(pa));
         for (int n = 0; n < n_runs; ++n) {
-            // software pipeline: next word and its first pair
-            const uint2 wn = pw[n + 1];
-            const double2 a0n = pa[wn.x & 0x3FFu];
+            const uint2 wn = pw[n + 1];  // software pipeline: the next run's word
             const int off = static_cast<int>(w.x & 0x3FFu);
             const int R = static_cast<int>((w.x >> 11) & 0xFFFu);
             const int s = static_cast<int>(w.y & 0xFFFu);
@@ -179,36 +178,12 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
                     ts[p] = c;
                 }
             }
-            // leaf run z = sum_{b<R} alpha'[b] c_b: Duff's device over pairs, a jump
-            // table executes exactly the run's pairs
-            const double2* ra = pa + off;
+            // leaf run z = sum_{b<R} alpha'[b] c_b: one brx.idx into a PTX Duff chain
             double z0[P], z1[P];
-#pragma unroll
-            for (int p = 0; p < P; ++p) {
-                z0[p] = a0.x * leaf[p][0];
-                z1[p] = a0.y * leaf[p][1];
-            }
-            const int np = min((R + 1) >> 1, LT / 2);
-#define QRMC_LEAF_PAIR(i)                                          \
-    case (i) + 1:                                                  \
-        if constexpr ((i) < LT / 2 && (i) > 0) {                   \
-            const double2 aa = ra[(i)];                            \
-            _Pragma("unroll") for (int p = 0; p < P; ++p) {        \
-                z0[p] = fma(aa.x, leaf[p][2 * (i)], z0[p]);        \
-                z1[p] = fma(aa.y, leaf[p][2 * (i) + 1], z1[p]);    \
-            }                                                      \
-        }                                                          \
-        [[fallthrough]];
-            switch (np) {
-                QRMC_LEAF_PAIR(15) QRMC_LEAF_PAIR(14) QRMC_LEAF_PAIR(13) QRMC_LEAF_PAIR(12)
-                QRMC_LEAF_PAIR(11) QRMC_LEAF_PAIR(10) QRMC_LEAF_PAIR(9) QRMC_LEAF_PAIR(8)
-                QRMC_LEAF_PAIR(7) QRMC_LEAF_PAIR(6) QRMC_LEAF_PAIR(5) QRMC_LEAF_PAIR(4)
-                QRMC_LEAF_PAIR(3) QRMC_LEAF_PAIR(2) QRMC_LEAF_PAIR(1)
-                default: break;
-            }
-#undef QRMC_LEAF_PAIR
+            leaf_chain<P, LT>(pa_s + 16u * static_cast<unsigned>(off), min((R + 1) >> 1, LT / 2), leaf, z0, z1);
             if (R > LT) {
                 // long run: continue the Chebyshev recurrence from (c_{LT-2}, c_{LT-1})
+                const double2* ra = pa + off;
                 double cp[P], cc[P];
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
@@ -235,7 +210,6 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
                 acc2[p] = fma(ts[p], z1[p], acc2[p]);
             }
             w = wn;
-            a0 = a0n;
         }
         __syncthreads();  // the buffer is refilled by the next iteration's prefetch
     }
