@@ -263,36 +263,52 @@ Program build_program(const Gamma& g) {
         r = e;
     }
 
-    // 3. tiles of whole runs: one 64-bit word per run (series_block.cuh), each
-    // tile's words followed by a zero word for the pipelined prefetch
+    // 3. tiles (series_block.cuh): per group chunk a header word, then one word
+    // per run; runs never split, groups continue across tiles
+    constexpr int kTileW = 1536;  // == kTileW in series_block.cuh
     int4 cur = make_int4(0, 0, 0, 0);
     int64_t alpha_pos = 0;
     auto close = [&] {
         if (cur.y == 0) return;
         p.tiles.push_back(cur);
-        p.tile_prog.push_back(0);
-        p.tile_prog.push_back(0);
         while (p.tile_prog.size() % 4) p.tile_prog.push_back(0);
     };
     auto open = [&] { cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0); };
     open();
+    const int LT = k1_lt(d);
     for (const Group& gr : groups) {
-        for (size_t s = 0; s < gr.n; ++s) {
-            const int64_t R = runs[gr.r0 + s].R;
-            const int64_t pad = (R + 1) & ~int64_t{1};
-            if (pad > kHostTileA || R >= 4096 || s >= 4096)
-                fail(QRMC_ENOTIMPL, fmt("leaf run of %lld coefficients exceeds a shared-memory tile", (long long)R));
-            if (cur.w + pad > kHostTileA || cur.y + 1 > kHostTileP) {
+        size_t s = 0;
+        while (s < gr.n) {
+            const int64_t R0 = runs[gr.r0 + s].R;
+            const int64_t pad0 = (R0 + 1) & ~int64_t{1};
+            if (pad0 > kHostTileA || R0 >= 4096)
+                fail(QRMC_ENOTIMPL, fmt("leaf run of %lld coefficients exceeds a shared-memory tile", (long long)R0));
+            if (cur.w + pad0 > kHostTileA || cur.y + 2 > kTileW) {
                 close();
                 open();
             }
-            const uint32_t x = static_cast<uint32_t>(cur.w / 2) | (static_cast<uint32_t>(R) << 11);
-            const uint32_t y = static_cast<uint32_t>(s) | (s == 0 ? (1u << 12) | (gr.L << 13) : 0u);
-            p.tile_prog.push_back(x);
-            p.tile_prog.push_back(y);
+            const size_t hdr_at = p.tile_prog.size();
+            p.tile_prog.push_back(0);
             cur.y += 1;
-            cur.w += static_cast<int>(pad);
-            alpha_pos += pad;
+            size_t take = 0;
+            while (s + take < gr.n) {
+                const int64_t R = runs[gr.r0 + s + take].R;
+                const int64_t pad = (R + 1) & ~int64_t{1};
+                if (pad > kHostTileA || R >= 4096)
+                    fail(QRMC_ENOTIMPL, fmt("leaf run of %lld coefficients exceeds a shared-memory tile", (long long)R));
+                if (cur.w + pad > kHostTileA || cur.y + 1 > kTileW || take >= 0xFFF) break;
+                const int64_t jm = std::min<int64_t>((R + 1) >> 1, LT / 2) - 1;
+                p.tile_prog.push_back(static_cast<uint32_t>(cur.w / 2) | (static_cast<uint32_t>(jm) << 10) |
+                                      (static_cast<uint32_t>(R) << 16));
+                cur.y += 1;
+                cur.w += static_cast<int>(pad);
+                alpha_pos += pad;
+                ++take;
+            }
+            const bool cont = s > 0;
+            p.tile_prog[hdr_at] = static_cast<uint32_t>(take) | ((cont ? 0u : gr.L) << 12) |
+                                  (static_cast<uint32_t>(s) << 16) | (cont ? (1u << 28) : 0u);
+            s += take;
         }
     }
     close();

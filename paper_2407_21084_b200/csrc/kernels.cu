@@ -48,11 +48,23 @@ __device__ __forceinline__ void sample_start(const MeasureDev& m, int d, Stream&
 // per dimension: k1_p / k1_s2 / k1_lt (qrmc_types.h).
 constexpr int kK1Threads = 128;
 
-// dynamic shared memory of a series kernel: coefficient/program tiles + the
-// per-thread sibling table c_{D-2}[0..S2) for P points
+// Per-path state of K1 kept in shared memory between evaluations, so the
+// series evaluation has the register file to itself.
 template <int D>
-constexpr size_t series_smem_bytes(int P) {
-    return sizeof(SeriesSmem) + static_cast<size_t>(k1_s2(D)) * P * kK1Threads * sizeof(double);
+struct PathSmem {
+    double xj[D];  // X_j
+    double xn[D];  // X_{j+1}
+    double w0, dsum;
+    unsigned long long block, buf1;  // RngStream position
+    int pos, bad;
+};
+
+// dynamic shared memory of a series kernel: coefficient/program tiles, the
+// per-thread sibling table c_{D-2}[0..S2) for P points, and (K1) path state
+template <int D>
+constexpr size_t series_smem_bytes(int P, bool paths = false) {
+    return sizeof(SeriesSmem) + static_cast<size_t>(k1_s2(D)) * P * kK1Threads * sizeof(double) +
+           (paths ? sizeof(PathSmem<D>) * P * kK1Threads : 0);
 }
 
 template <int D>
@@ -61,79 +73,102 @@ __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
     extern __shared__ __align__(16) unsigned char dsm[];
     SeriesSmem& sm = *reinterpret_cast<SeriesSmem*>(dsm);
     double* t2s = reinterpret_cast<double*>(dsm + sizeof(SeriesSmem));
+    PathSmem<D>* ps = reinterpret_cast<PathSmem<D>*>(dsm + sizeof(SeriesSmem) +
+                                                    static_cast<size_t>(S2) * P * kK1Threads * sizeof(double));
     __shared__ int s_abort;
     if (threadIdx.x == 0) s_abort = *a.abort_flag;
     __syncthreads();
     if (s_abort) return;  // uniform per CTA
 
-    int64_t q[P];
-    bool valid[P];
-    double xj[P][D], xn[P][D], w0[P], dsum[P];
-    int bad[P];
     uint32_t apps = 0, clipped = 0;
-    Stream st_p[P];
+    int64_t m_of[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-        q[p] = (static_cast<int64_t>(blockIdx.x) * P + p) * kK1Threads + threadIdx.x;
-        valid[p] = q[p] < a.n_owned;
-        const int64_t qq = valid[p] ? q[p] : 0;
-        const int64_t m = owned_to_path(a, qq);
-        st_p[p] = Stream(a.seed, sid_training(a.step, static_cast<uint64_t>(m)));
+        PathSmem<D>& st = ps[p * kK1Threads + threadIdx.x];
+        const int64_t q = (static_cast<int64_t>(blockIdx.x) * P + p) * kK1Threads + threadIdx.x;
+        const bool valid = q < a.n_owned;
+        m_of[p] = owned_to_path(a, valid ? q : 0);
+        Stream s(a.seed, sid_training(a.step, static_cast<uint64_t>(m_of[p])));
+        double x[D];
 #pragma unroll
-        for (int l = 0; l < D; ++l) xj[p][l] = measure_inv_cdf(a.meas, st_p[p].next_uniform(), l);
-        w0[p] = damping_weight<D>(xj[p], a.q);
-        if (a.cloud && valid[p]) {
+        for (int l = 0; l < D; ++l) x[l] = measure_inv_cdf(a.meas, s.next_uniform(), l);
+        if (a.cloud && valid) {
 #pragma unroll
-            for (int l = 0; l < D; ++l) a.cloud[l * a.n_owned + q[p]] = xj[p][l];
+            for (int l = 0; l < D; ++l) a.cloud[l * a.n_owned + q] = x[l];
         }
-        dsum[p] = 0.0;
-        bad[p] = 0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) st.xj[l] = x[l];
+        st.w0 = damping_weight<D>(x, a.q);
+        st.dsum = 0.0;
+        st.block = s.block;
+        st.buf1 = s.buf1;
+        st.pos = s.pos;
+        st.bad = 0;
     }
     for (int j = a.step; j < a.steps; ++j) {
-        double y[P];
+        const bool last = j + 1 == a.steps;
+        double c1[P][D];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
+            PathSmem<D>& st = ps[p * kK1Threads + threadIdx.x];
+            Stream s(a.seed, sid_training(a.step, static_cast<uint64_t>(m_of[p])));
+            s.block = st.block;
+            s.buf1 = st.buf1;
+            s.pos = st.pos;
+            double x[D];
 #pragma unroll
-            for (int l = 0; l < D; ++l) xn[p][l] = xj[p][l];
-            const int b = euler_step<D>(a.prob, xn[p], a.sqrt_dt, a.dt, st_p[p], j);
-            if (b && !bad[p]) bad[p] = b;
+            for (int l = 0; l < D; ++l) x[l] = st.xj[l];
+            const int b = euler_step<D>(a.prob, x, a.sqrt_dt, a.dt, s, j);
+            if (b && !st.bad) st.bad = b;
+            st.block = s.block;
+            st.buf1 = s.buf1;
+            st.pos = s.pos;
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                st.xn[l] = x[l];
+                c1[p][l] = last ? 0.0 : cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, x[l], l)));
+            }
         }
-        if (j + 1 == a.steps) {
-#pragma unroll
-            for (int p = 0; p < P; ++p) y[p] = terminal<D>(a.prob, xn[p]);  // exact initialisation (solver.cpp:69-72)
-        } else {
-            double c1[P][D], ys[P];
-#pragma unroll
-            for (int p = 0; p < P; ++p)
-#pragma unroll
-                for (int l = 0; l < D; ++l)
-                    c1[p][l] = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xn[p][l], l)));
+        double ys[P];
+        if (!last)
             series_block<D, P, S2, LT>(sm, t2s, a.tiles, a.alpha_packed + static_cast<int64_t>(j + 1) * a.kp, c1, ys);
 #pragma unroll
-            for (int p = 0; p < P; ++p) y[p] = DMUL(ys[p], damping_weight<D>(xn[p], a.q));
-        }
-#pragma unroll
         for (int p = 0; p < P; ++p) {
-            const double c = truncate_soft(y[p], lstar<D>(a.prob, xn[p]));
-            if (valid[p]) {
-                ++apps;
-                if (c != y[p]) ++clipped;
-            }
-            dsum[p] = DADD(dsum[p], driver<D>(a.prob, DMUL(static_cast<double>(j), a.dt), xj[p], c));
+            PathSmem<D>& st = ps[p * kK1Threads + threadIdx.x];
+            const int64_t q = (static_cast<int64_t>(blockIdx.x) * P + p) * kK1Threads + threadIdx.x;
+            double xn[D], xj[D];
 #pragma unroll
-            for (int l = 0; l < D; ++l) xj[p][l] = xn[p][l];
+            for (int l = 0; l < D; ++l) {
+                xn[l] = st.xn[l];
+                xj[l] = st.xj[l];
+            }
+            // exact initialisation at the terminal step (solver.cpp:69-72)
+            const double y = last ? terminal<D>(a.prob, xn) : DMUL(ys[p], damping_weight<D>(xn, a.q));
+            const double c = truncate_soft(y, lstar<D>(a.prob, xn));
+            if (q < a.n_owned) {
+                ++apps;
+                if (c != y) ++clipped;
+            }
+            st.dsum = DADD(st.dsum, driver<D>(a.prob, DMUL(static_cast<double>(j), a.dt), xj, c));
+#pragma unroll
+            for (int l = 0; l < D; ++l) st.xj[l] = xn[l];
         }
     }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-        if (!valid[p]) continue;
-        if (bad[p]) {
-            record_error(a.err_flags, QRMC_ESIM, bad[p]);
+        const int64_t q = (static_cast<int64_t>(blockIdx.x) * P + p) * kK1Threads + threadIdx.x;
+        if (q >= a.n_owned) continue;
+        const PathSmem<D>& st = ps[p * kK1Threads + threadIdx.x];
+        if (st.bad) {
+            record_error(a.err_flags, QRMC_ESIM, st.bad);
         } else {
-            const double term = terminal<D>(a.prob, xj[p]);
-            const double v = DDIV(DADD(term, DMUL(a.dt, dsum[p])), w0[p]);
+            double xj[D];
+#pragma unroll
+            for (int l = 0; l < D; ++l) xj[l] = st.xj[l];
+            const double term = terminal<D>(a.prob, xj);
+            const double v = DDIV(DADD(term, DMUL(a.dt, st.dsum)), st.w0);
             if (!isfinite(v)) record_error(a.err_flags, QRMC_ENUMERIC, 0);
-            a.resp[q[p]] = v;
+            a.resp[q] = v;
         }
     }
     // truncation counters: warp-aggregate then one atomic per warp
@@ -372,7 +407,7 @@ cudaError_t configure_series_kernels() {
                 e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
         };
 #define QRMC_CONFIGURE(Dv)                                                                           \
-    set(reinterpret_cast<const void*>(&k_responses<Dv>), series_smem_bytes<Dv>(k1_p(Dv)));          \
+    set(reinterpret_cast<const void*>(&k_responses<Dv>), series_smem_bytes<Dv>(k1_p(Dv), true));          \
     set(reinterpret_cast<const void*>(&k_eval_points<Dv>), series_smem_bytes<Dv>(1));              \
     set(reinterpret_cast<const void*>(&k_mse<Dv>), series_smem_bytes<Dv>(1));
         QRMC_CONFIGURE(1) QRMC_CONFIGURE(2) QRMC_CONFIGURE(3) QRMC_CONFIGURE(4)
@@ -388,7 +423,7 @@ cudaError_t launch_responses(const StepArgs& a, cudaStream_t st) {
     QRMC_DISPATCH_D(a.prob.dim, {
         const int64_t per_cta = static_cast<int64_t>(kK1Threads) * k1_p(D);
         const unsigned blocks = static_cast<unsigned>((a.n_owned + per_cta - 1) / per_cta);
-        k_responses<D><<<blocks, kK1Threads, series_smem_bytes<D>(k1_p(D)), st>>>(a);
+        k_responses<D><<<blocks, kK1Threads, series_smem_bytes<D>(k1_p(D), true), st>>>(a);
     });
     return cudaGetLastError();
 }

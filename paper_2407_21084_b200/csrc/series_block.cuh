@@ -13,16 +13,15 @@
 // the tables continue that recurrence in registers. Levels above D-2 change
 // rarely and carry (2c1, c_prev, c_cur, acc) recurrence state.
 //
-// Program (host.cpp build_program): one 64-bit word per leaf run,
-//   x: bits 0..10  pair offset of the run's coefficients inside the tile
-//      bits 11..22 run length R
-//   y: bits 0..11  sibling index s = k_{D-2}
-//      bit  12     first run of a group (upper prefix k_0..k_{D-3} changed)
-//      bits 13..16 transition level L of that prefix change (15: first group)
-// cut into tiles of <= kTileA coefficients / <= kTileP runs that stream
-// through shared memory with cp.async double buffering. The node loop is
-// software-pipelined: the next run's word and first coefficient pair are
-// loaded while the current run computes. Control flow is uniform across the
+// Program (host.cpp build_program): a stream of 32-bit words per tile,
+//   group header: bits 0..11 runs n in this chunk, 12..15 transition level L
+//                 of the upper prefix (15: first group), 16..27 first sibling
+//                 index s0, bit 28: continuation of the previous tile's group
+//   run word:     bits 0..9 pair offset of the coefficients inside the tile,
+//                 10..13 (pairs in the register table) - 1, 16..27 run length R
+// with the runs of a group in sibling order s = s0, s0+1, ...; tiles hold
+// <= kTileA coefficients and <= kTileW words and stream through shared
+// memory with cp.async double buffering. Control flow is uniform across the
 // CTA (every thread walks the same program), so it never diverges.
 #pragma once
 
@@ -34,12 +33,12 @@
 namespace qrmc_dev {
 
 constexpr int kTileA = 2048;    // coefficients per shared-memory tile (16 KiB)
-constexpr int kTileP = 1024;    // runs per tile (8 KiB of words)
+constexpr int kTileW = 1536;    // program words per tile (6 KiB)
 constexpr int kFirstGroup = 15; // transition code of the first group
 
 struct SeriesSmem {
     double alpha[2][kTileA + 8];  // +8: the leaf chain preloads 4 pairs, possibly past a tile's end
-    uint2 prog[2][kTileP + 2];    // + a zero word after the last run (pipelined prefetch)
+    uint32_t prog[2][kTileW + 4];
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -56,9 +55,9 @@ __device__ __forceinline__ void load_tile(SeriesSmem& sm, int buf, const SeriesT
     const int na = d.w >> 1;  // 16-byte chunks of coefficients
     const double* ga = row + d.z;
     for (int c = threadIdx.x; c < na; c += blockDim.x) cp_async16(&sm.alpha[buf][2 * c], ga + 2 * c);
-    const int np = (d.y + 2) >> 1;  // two 8-byte words per chunk, incl. the zero pad word
+    const int np = (d.y + 3) >> 2;  // four words per 16-byte chunk
     const uint32_t* gp = st.prog + d.x;
-    for (int c = threadIdx.x; c < np; c += blockDim.x) cp_async16(&sm.prog[buf][2 * c], gp + 4 * c);
+    for (int c = threadIdx.x; c < np; c += blockDim.x) cp_async16(&sm.prog[buf][4 * c], gp + 4 * c);
 }
 
 // Evaluate the series of coefficient row `row` at P points per thread.
@@ -117,20 +116,19 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
             cp_async_wait<0>();
         }
         __syncthreads();
-        const int n_runs = st.tiles[t].y;
-        const uint2* pw = sm.prog[buf];
+        const int n_words = st.tiles[t].y;
+        const uint32_t* pw = sm.prog[buf];
         const double2* pa = reinterpret_cast<const double2*>(sm.alpha[buf]);
-        uint2 w = pw[0];  // pair offsets are < 1024 (masked 0x3FF)
         const unsigned pa_s = static_cast<unsigned>(__cvta_generic_to_shared(pa));
-        for (int n = 0; n < n_runs; ++n) {
-            const uint2 wn = pw[n + 1];  // software pipeline: the next run's word
-            const int off = static_cast<int>(w.x & 0x3FFu);
-            const int R = static_cast<int>((w.x >> 11) & 0xFFFu);
-            const int s = static_cast<int>(w.y & 0xFFFu);
-            if (w.y & 0x1000u) {
-                // first run of a group: close the previous group and the upper nodes
-                // above it, advance level L of the upper prefix
-                const int L = static_cast<int>((w.y >> 13) & 15u);
+        int i = 0;
+        while (i < n_words) {
+            const uint32_t h = pw[i++];
+            const int n = static_cast<int>(h & 0xFFFu);
+            const int s0 = static_cast<int>((h >> 16) & 0xFFFu);
+            if (!(h & (1u << 28))) {
+                // a new group: close the previous one and the upper nodes above it,
+                // advance level L of the upper prefix
+                const int L = static_cast<int>((h >> 12) & 15u);
                 if constexpr (D > 2) {
                     if (L != kFirstGroup) {
 #pragma unroll
@@ -164,52 +162,57 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
                     g2c[p] = t2s[((S2 - 1) * P + p) * nt + tid];
                 }
             }
-            // sibling weight c_{D-2}[s]
-            double ts[P];
-            if (s < S2) {
+            const uint32_t* runs = pw + i;
+            i += n;
+            for (int k = 0; k < n; ++k) {
+                const uint32_t r = runs[k];
+                const int s = s0 + k;
+                // sibling weight c_{D-2}[s]
+                double ts[P];
+                if (s < S2) {
 #pragma unroll
-                for (int p = 0; p < P; ++p) ts[p] = t2s[(s * P + p) * nt + tid];
-            } else {
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const double c = fma(t2c[p], g2c[p], -g2p[p]);
-                    g2p[p] = g2c[p];
-                    g2c[p] = c;
-                    ts[p] = c;
-                }
-            }
-            // leaf run z = sum_{b<R} alpha'[b] c_b: one brx.idx into a PTX Duff chain
-            double z0[P], z1[P];
-            leaf_chain<P, LT>(pa_s + 16u * static_cast<unsigned>(off), min((R + 1) >> 1, LT / 2), leaf, z0, z1);
-            if (R > LT) {
-                // long run: continue the Chebyshev recurrence from (c_{LT-2}, c_{LT-1})
-                const double2* ra = pa + off;
-                double cp[P], cc[P];
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    cp[p] = leaf[p][LT - 2];
-                    cc[p] = leaf[p][LT - 1];
-                }
-                const int pairs = (R + 1) >> 1;
-                for (int b2 = LT / 2; b2 < pairs; ++b2) {
-                    const double2 aa = ra[b2];
+                    for (int p = 0; p < P; ++p) ts[p] = t2s[(s * P + p) * nt + tid];
+                } else {
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
-                        const double e = fma(tl[p], cc[p], -cp[p]);  // c_{2 b2}
-                        const double o = fma(tl[p], e, -cc[p]);      // c_{2 b2 + 1}
-                        z0[p] = fma(aa.x, e, z0[p]);
-                        z1[p] = fma(aa.y, o, z1[p]);
-                        cp[p] = e;
-                        cc[p] = o;
+                        const double c = fma(t2c[p], g2c[p], -g2p[p]);
+                        g2p[p] = g2c[p];
+                        g2c[p] = c;
+                        ts[p] = c;
                     }
                 }
-            }
+                // leaf run z = sum_{b<R} alpha'[b] c_b: one brx.idx into a PTX Duff chain
+                const int off = static_cast<int>(r & 0x3FFu);
+                double z[P];
+                leaf_chain<P, LT>(pa_s + 16u * static_cast<unsigned>(off), static_cast<int>((r >> 10) & 15u) + 1,
+                                  leaf, z);
+                const int R = static_cast<int>(r >> 16);
+                if (R > LT) {
+                    // long run: continue the Chebyshev recurrence from (c_{LT-2}, c_{LT-1})
+                    const double2* ra = pa + off;
+                    double cp[P], cc[P];
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                acc2[p] = fma(ts[p], z0[p], acc2[p]);
-                acc2[p] = fma(ts[p], z1[p], acc2[p]);
+                    for (int p = 0; p < P; ++p) {
+                        cp[p] = leaf[p][LT - 2];
+                        cc[p] = leaf[p][LT - 1];
+                    }
+                    const int pairs = (R + 1) >> 1;
+                    for (int b2 = LT / 2; b2 < pairs; ++b2) {
+                        const double2 aa = ra[b2];
+#pragma unroll
+                        for (int p = 0; p < P; ++p) {
+                            const double e = fma(tl[p], cc[p], -cp[p]);  // c_{2 b2}
+                            const double o = fma(tl[p], e, -cc[p]);      // c_{2 b2 + 1}
+                            z[p] = fma(aa.x, e, z[p]);
+                            z[p] = fma(aa.y, o, z[p]);
+                            cp[p] = e;
+                            cc[p] = o;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < P; ++p) acc2[p] = fma(ts[p], z[p], acc2[p]);
             }
-            w = wn;
         }
         __syncthreads();  // the buffer is refilled by the next iteration's prefetch
     }
