@@ -21,7 +21,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libqrmc_gpu.so"
 SOURCES = [CSRC / "kernels.cu", CSRC / "host.cpp"]
-HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "series_block.cuh", CSRC / "leaf_chain.cuh", ROOT / "include" / "qrmc_gpu.h",
+HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "series_block.cuh", ROOT / "include" / "qrmc_gpu.h",
            ROOT / "include" / "qrmc_normal_quantile.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

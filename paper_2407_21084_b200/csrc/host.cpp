@@ -264,7 +264,8 @@ Program build_program(const Gamma& g) {
     }
 
     // 3. tiles (series_block.cuh): per group chunk a header word, then one word
-    // per run; runs never split, groups continue across tiles
+    // per segment of consecutive equal-length runs; runs never split, groups
+    // and segments continue across tiles
     constexpr int kTileW = 1536;  // == kTileW in series_block.cuh
     int4 cur = make_int4(0, 0, 0, 0);
     int64_t alpha_pos = 0;
@@ -275,7 +276,6 @@ Program build_program(const Gamma& g) {
     };
     auto open = [&] { cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0); };
     open();
-    const int LT = k1_lt(d);
     for (const Group& gr : groups) {
         size_t s = 0;
         while (s < gr.n) {
@@ -288,27 +288,33 @@ Program build_program(const Gamma& g) {
                 open();
             }
             const size_t hdr_at = p.tile_prog.size();
+            const size_t s_first = s;
             p.tile_prog.push_back(0);
             cur.y += 1;
-            size_t take = 0;
-            while (s + take < gr.n) {
-                const int64_t R = runs[gr.r0 + s + take].R;
+            uint32_t n_seg = 0;
+            // segments while the tile has room
+            while (s < gr.n && cur.y + 1 <= kTileW && n_seg < 0xFFF) {
+                const int64_t R = runs[gr.r0 + s].R;
                 const int64_t pad = (R + 1) & ~int64_t{1};
                 if (pad > kHostTileA || R >= 4096)
                     fail(QRMC_ENOTIMPL, fmt("leaf run of %lld coefficients exceeds a shared-memory tile", (long long)R));
-                if (cur.w + pad > kHostTileA || cur.y + 1 > kTileW || take >= 0xFFF) break;
-                const int64_t jm = std::min<int64_t>((R + 1) >> 1, LT / 2) - 1;
-                p.tile_prog.push_back(static_cast<uint32_t>(cur.w / 2) | (static_cast<uint32_t>(jm) << 10) |
-                                      (static_cast<uint32_t>(R) << 16));
+                if (cur.w + pad > kHostTileA) break;
+                int64_t cnt = 0;
+                const int first_pair = cur.w / 2;
+                while (s < gr.n && runs[gr.r0 + s].R == R && cur.w + pad <= kHostTileA && cnt < 1023) {
+                    cur.w += static_cast<int>(pad);
+                    alpha_pos += pad;
+                    ++cnt;
+                    ++s;
+                }
+                p.tile_prog.push_back(static_cast<uint32_t>(first_pair) | (static_cast<uint32_t>(R) << 10) |
+                                      (static_cast<uint32_t>(cnt) << 22));
                 cur.y += 1;
-                cur.w += static_cast<int>(pad);
-                alpha_pos += pad;
-                ++take;
+                ++n_seg;
             }
-            const bool cont = s > 0;
-            p.tile_prog[hdr_at] = static_cast<uint32_t>(take) | ((cont ? 0u : gr.L) << 12) |
-                                  (static_cast<uint32_t>(s) << 16) | (cont ? (1u << 28) : 0u);
-            s += take;
+            const bool cont = s_first > 0;
+            p.tile_prog[hdr_at] = n_seg | ((cont ? 0u : gr.L) << 12) | (static_cast<uint32_t>(s_first) << 16) |
+                                  (cont ? (1u << 28) : 0u);
         }
     }
     close();

@@ -6,29 +6,29 @@
 // and alpha'_k = alpha_k sqrt2^{nnz(k)} (packed by host.cpp):
 //     y = sum_{upper prefix} (prod_{l<D-2} c_l) sum_s c_{D-2}[s] sum_b alpha'[.., s, b] c_{D-1}[b]
 // Leaf values c_{D-1}[0..LT) live in a per-point REGISTER table (static
-// indices inside a Duff's-device jump table, so a run of R coefficients costs
-// exactly R FMAs), sibling weights c_{D-2}[0..S2) in a per-thread SHARED
+// indices: the run length is static inside a segment loop), sibling weights c_{D-2}[0..S2) in a per-thread SHARED
 // table (one LDS per run), both computed once per evaluation with the
 // reference's three-term recurrence (cosine_basis.cpp:79-86); indices past
 // the tables continue that recurrence in registers. Levels above D-2 change
 // rarely and carry (2c1, c_prev, c_cur, acc) recurrence state.
 //
 // Program (host.cpp build_program): a stream of 32-bit words per tile,
-//   group header: bits 0..11 runs n in this chunk, 12..15 transition level L
-//                 of the upper prefix (15: first group), 16..27 first sibling
-//                 index s0, bit 28: continuation of the previous tile's group
-//   run word:     bits 0..9 pair offset of the coefficients inside the tile,
-//                 10..13 (pairs in the register table) - 1, 16..27 run length R
-// with the runs of a group in sibling order s = s0, s0+1, ...; tiles hold
-// <= kTileA coefficients and <= kTileW words and stream through shared
-// memory with cp.async double buffering. Control flow is uniform across the
+//   group header: bits 0..11 number of segments, 12..15 transition level L of
+//                 the upper prefix (15: first group), 16..27 first sibling s0,
+//                 bit 28: continuation of the previous tile's group
+//   segment word: bits 0..9 pair offset of its coefficients in the tile,
+//                 10..21 run length R, 22..31 number of runs (consecutive
+//                 siblings whose leaf runs all have length R)
+// One dispatch per segment into a loop whose body is static for R <= LT, so
+// a run costs R FMAs + 1 fold per point and a few loads. Tiles hold <= kTileA
+// coefficients and <= kTileW words and stream through shared memory with
+// cp.async double buffering. Control flow is uniform across the
 // CTA (every thread walks the same program), so it never diverges.
 #pragma once
 
 #include <cstdint>
 
 #include "kernels.cuh"
-#include "leaf_chain.cuh"
 
 namespace qrmc_dev {
 
@@ -59,6 +59,101 @@ __device__ __forceinline__ void load_tile(SeriesSmem& sm, int buf, const SeriesT
     const uint32_t* gp = st.prog + d.x;
     for (int c = threadIdx.x; c < np; c += blockDim.x) cp_async16(&sm.prog[buf][4 * c], gp + 4 * c);
 }
+
+// The sibling runs of one segment: cnt consecutive siblings s, s+1, ... whose
+// leaf runs all have length R; coefficients contiguous, each run padded to even.
+template <int P, int S2, int LT>
+struct SegState {
+    const double (&leaf)[P][LT];
+    const double (&tl)[P];
+    const double (&t2c)[P];
+    const double* t2 /* t2s + tid */;
+    int nt;
+    double (&g2p)[P];
+    double (&g2c)[P];
+    double (&acc2)[P];
+
+    // sibling weight c_{D-2}[s]: shared table below S2, recurrence (in order) above
+    __device__ __forceinline__ void weight(int s, double (&ts)[P]) {
+        if (s < S2) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) ts[p] = t2[(s * P + p) * nt];
+        } else {
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const double c = fma(t2c[p], g2c[p], -g2p[p]);
+                g2p[p] = g2c[p];
+                g2c[p] = c;
+                ts[p] = c;
+            }
+        }
+    }
+
+    // R <= LT: fully static run body, R FMAs + 1 fold per point per run
+    template <int R>
+    __device__ __forceinline__ void run_fixed(const double2* ra, int s, int cnt) {
+        constexpr int NP = (R + 1) / 2;
+#pragma unroll 2
+        for (int k = 0; k < cnt; ++k, ra += NP) {
+            double ts[P];
+            weight(s + k, ts);
+            double z[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) z[p] = 0.0;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                const double2 a = ra[j];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    z[p] = fma(a.x, leaf[p][2 * j], z[p]);
+                    if (2 * j + 1 < R) z[p] = fma(a.y, leaf[p][2 * j + 1], z[p]);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) acc2[p] = fma(ts[p], z[p], acc2[p]);
+        }
+    }
+
+    // R > LT: the register table, then the Chebyshev recurrence (2 FMAs per term)
+    __device__ __forceinline__ void run_long(const double2* ra, int R, int s, int cnt) {
+        const int np = (R + 1) >> 1;
+        for (int k = 0; k < cnt; ++k, ra += np) {
+            double ts[P];
+            weight(s + k, ts);
+            double z[P], cp[P], cc[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) z[p] = 0.0;
+#pragma unroll
+            for (int j = 0; j < LT / 2; ++j) {
+                const double2 a = ra[j];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    z[p] = fma(a.x, leaf[p][2 * j], z[p]);
+                    z[p] = fma(a.y, leaf[p][2 * j + 1], z[p]);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                cp[p] = leaf[p][LT - 2];
+                cc[p] = leaf[p][LT - 1];
+            }
+            for (int j = LT / 2; j < np; ++j) {
+                const double2 a = ra[j];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double e = fma(tl[p], cc[p], -cp[p]);  // c_{2j}
+                    const double o = fma(tl[p], e, -cc[p]);      // c_{2j+1}
+                    z[p] = fma(a.x, e, z[p]);
+                    z[p] = fma(a.y, o, z[p]);
+                    cp[p] = e;
+                    cc[p] = o;
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) acc2[p] = fma(ts[p], z[p], acc2[p]);
+        }
+    }
+};
 
 // Evaluate the series of coefficient row `row` at P points per thread.
 // c1[p][l] = cos(pi u_l) of point p; t2s: shared scratch of S2*P*blockDim doubles.
@@ -119,12 +214,11 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
         const int n_words = st.tiles[t].y;
         const uint32_t* pw = sm.prog[buf];
         const double2* pa = reinterpret_cast<const double2*>(sm.alpha[buf]);
-        const unsigned pa_s = static_cast<unsigned>(__cvta_generic_to_shared(pa));
         int i = 0;
         while (i < n_words) {
             const uint32_t h = pw[i++];
-            const int n = static_cast<int>(h & 0xFFFu);
-            const int s0 = static_cast<int>((h >> 16) & 0xFFFu);
+            const int n_seg = static_cast<int>(h & 0xFFFu);
+            int s = static_cast<int>((h >> 16) & 0xFFFu);
             if (!(h & (1u << 28))) {
                 // a new group: close the previous one and the upper nodes above it,
                 // advance level L of the upper prefix
@@ -162,56 +256,28 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
                     g2c[p] = t2s[((S2 - 1) * P + p) * nt + tid];
                 }
             }
-            const uint32_t* runs = pw + i;
-            i += n;
-            for (int k = 0; k < n; ++k) {
-                const uint32_t r = runs[k];
-                const int s = s0 + k;
-                // sibling weight c_{D-2}[s]
-                double ts[P];
-                if (s < S2) {
-#pragma unroll
-                    for (int p = 0; p < P; ++p) ts[p] = t2s[(s * P + p) * nt + tid];
-                } else {
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        const double c = fma(t2c[p], g2c[p], -g2p[p]);
-                        g2p[p] = g2c[p];
-                        g2c[p] = c;
-                        ts[p] = c;
-                    }
+            SegState<P, S2, LT> ss{leaf, tl, t2c, t2s + tid, nt, g2p, g2c, acc2};
+            for (int g = 0; g < n_seg; ++g) {
+                const uint32_t w = pw[i++];
+                const double2* ra = pa + (w & 0x3FFu);
+                const int R = static_cast<int>((w >> 10) & 0xFFFu);
+                const int cnt = static_cast<int>(w >> 22);
+                // one dispatch per segment of equal-length runs
+                switch (R) {
+#define QRMC_SEG(r) \
+    case r:         \
+        if constexpr ((r) <= LT) ss.template run_fixed<(r)>(ra, s, cnt); \
+        break;
+                    QRMC_SEG(1) QRMC_SEG(2) QRMC_SEG(3) QRMC_SEG(4) QRMC_SEG(5) QRMC_SEG(6) QRMC_SEG(7)
+                    QRMC_SEG(8) QRMC_SEG(9) QRMC_SEG(10) QRMC_SEG(11) QRMC_SEG(12) QRMC_SEG(13) QRMC_SEG(14)
+                    QRMC_SEG(15) QRMC_SEG(16) QRMC_SEG(17) QRMC_SEG(18) QRMC_SEG(19) QRMC_SEG(20) QRMC_SEG(21)
+                    QRMC_SEG(22) QRMC_SEG(23) QRMC_SEG(24) QRMC_SEG(25) QRMC_SEG(26) QRMC_SEG(27) QRMC_SEG(28)
+                    QRMC_SEG(29) QRMC_SEG(30) QRMC_SEG(31) QRMC_SEG(32)
+#undef QRMC_SEG
+                    default: break;
                 }
-                // leaf run z = sum_{b<R} alpha'[b] c_b: one brx.idx into a PTX Duff chain
-                const int off = static_cast<int>(r & 0x3FFu);
-                double z[P];
-                leaf_chain<P, LT>(pa_s + 16u * static_cast<unsigned>(off), static_cast<int>((r >> 10) & 15u) + 1,
-                                  leaf, z);
-                const int R = static_cast<int>(r >> 16);
-                if (R > LT) {
-                    // long run: continue the Chebyshev recurrence from (c_{LT-2}, c_{LT-1})
-                    const double2* ra = pa + off;
-                    double cp[P], cc[P];
-#pragma unroll
-                    for (int p = 0; p < P; ++p) {
-                        cp[p] = leaf[p][LT - 2];
-                        cc[p] = leaf[p][LT - 1];
-                    }
-                    const int pairs = (R + 1) >> 1;
-                    for (int b2 = LT / 2; b2 < pairs; ++b2) {
-                        const double2 aa = ra[b2];
-#pragma unroll
-                        for (int p = 0; p < P; ++p) {
-                            const double e = fma(tl[p], cc[p], -cp[p]);  // c_{2 b2}
-                            const double o = fma(tl[p], e, -cc[p]);      // c_{2 b2 + 1}
-                            z[p] = fma(aa.x, e, z[p]);
-                            z[p] = fma(aa.y, o, z[p]);
-                            cp[p] = e;
-                            cc[p] = o;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int p = 0; p < P; ++p) acc2[p] = fma(ts[p], z[p], acc2[p]);
+                if (R > LT) ss.run_long(ra, R, s, cnt);
+                s += cnt;
             }
         }
         __syncthreads();  // the buffer is refilled by the next iteration's prefetch
