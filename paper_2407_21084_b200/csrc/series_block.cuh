@@ -89,28 +89,48 @@ struct SegState {
         }
     }
 
-    // R <= LT: fully static run body, R FMAs + 1 fold per point per run
+    // R <= LT: fully static run body, R FMAs + 1 fold per point per run. The
+    // siblings below S2 (shared table) and above (recurrence) run as two loops
+    // so neither path is predicated into the other.
     template <int R>
     __device__ __forceinline__ void run_fixed(const double2* ra, int s, int cnt) {
         constexpr int NP = (R + 1) / 2;
-#pragma unroll 2
-        for (int k = 0; k < cnt; ++k, ra += NP) {
-            double ts[P];
-            weight(s + k, ts);
+        auto body = [&](const double (&ts)[P]) {
             double z[P];
-#pragma unroll
-            for (int p = 0; p < P; ++p) z[p] = 0.0;
 #pragma unroll
             for (int j = 0; j < NP; ++j) {
                 const double2 a = ra[j];
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
-                    z[p] = fma(a.x, leaf[p][2 * j], z[p]);
+                    z[p] = j == 0 ? a.x * leaf[p][0] : fma(a.x, leaf[p][2 * j], z[p]);
                     if (2 * j + 1 < R) z[p] = fma(a.y, leaf[p][2 * j + 1], z[p]);
                 }
             }
 #pragma unroll
             for (int p = 0; p < P; ++p) acc2[p] = fma(ts[p], z[p], acc2[p]);
+            ra += NP;
+        };
+        int n_tab = S2 - s;
+        n_tab = n_tab < 0 ? 0 : (n_tab > cnt ? cnt : n_tab);
+        const double* tp = t2 + s * P * nt;
+#pragma unroll 2
+        for (int k = 0; k < n_tab; ++k) {
+            double ts[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) ts[p] = tp[p * nt];
+            tp += P * nt;
+            body(ts);
+        }
+        for (int k = n_tab; k < cnt; ++k) {
+            double ts[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const double c = fma(t2c[p], g2c[p], -g2p[p]);
+                g2p[p] = g2c[p];
+                g2c[p] = c;
+                ts[p] = c;
+            }
+            body(ts);
         }
     }
 
