@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "_lib" / "libqrmc_gpu.so"
+LIB_PATH = Path(os.environ["QRMC_GPU_LIB"]) if os.environ.get("QRMC_GPU_LIB") else PKG_DIR / "_lib" / "libqrmc_gpu.so"
 
 # qrmc_status
 OK, EINVAL, ENUMERIC, ESIM, ECAPACITY, ECUDA, ENCCL, ENOTIMPL, ELOGIC = range(9)

@@ -40,14 +40,15 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS + [Path(__file__)])
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    target = out or OUT
+    if out is None and not force and not needs_build():
         return OUT
-    OUT.parent.mkdir(parents=True, exist_ok=True)
-    tmp = OUT.with_suffix(".so.tmp")
+    target.parent.mkdir(parents=True, exist_ok=True)
+    tmp = target.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}",
-           *map(str, SOURCES), "-o", str(tmp), "-ldl"]
+           *[f"-D{d}" for d in defines], *map(str, SOURCES), "-o", str(tmp), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -56,8 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr}")
     if verbose and r.stderr:
         print(r.stderr, file=sys.stderr)
-    tmp.replace(OUT)
-    return OUT
+    tmp.replace(target)
+    return target
 
 
 if __name__ == "__main__":

@@ -420,6 +420,51 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
 };
 
+// K2 work items: every leaf run cut into chunks of <= kProjRun terms, each with
+// the per-point table offsets of its prefix (k_0..k_{d-2}) and first leaf value
+// (cosine_basis.cpp:58-64 table layout); sorted by length so warps stay in step.
+struct ProjectItems {
+    std::vector<int32_t> k, len, leaf, pre;  // pre: [d-1][n]
+    int n = 0;
+};
+
+ProjectItems build_project_items(const Gamma& g, const int* offset) {
+    const int d = g.dim;
+    const int64_t K = g.size();
+    struct It { int32_t k, len, leaf; std::vector<int32_t> pre; };
+    std::vector<It> items;
+    for (int64_t i = 0; i < K;) {
+        int64_t j = i;
+        auto same = [&](int64_t r) {
+            for (int l = 0; l < d - 1; ++l)
+                if (g.rows[static_cast<size_t>(r * d + l)] != g.rows[static_cast<size_t>(i * d + l)]) return false;
+            return true;
+        };
+        while (j < K && same(j)) ++j;
+        for (int64_t b0 = i; b0 < j; b0 += kProjRun) {
+            It it;
+            it.k = static_cast<int32_t>(b0);
+            it.len = static_cast<int32_t>(std::min<int64_t>(kProjRun, j - b0));
+            it.leaf = offset[d - 1] + g.rows[static_cast<size_t>(b0 * d + d - 1)];
+            for (int l = 0; l < d - 1; ++l) it.pre.push_back(offset[l] + g.rows[static_cast<size_t>(b0 * d + l)]);
+            items.push_back(std::move(it));
+        }
+        i = j;
+    }
+    std::stable_sort(items.begin(), items.end(), [](const It& a, const It& b) { return a.len > b.len; });
+    ProjectItems out;
+    out.n = static_cast<int>(items.size());
+    const int np = std::max(d - 1, 1);
+    out.pre.assign(static_cast<size_t>(np) * out.n, 0);
+    for (int t = 0; t < out.n; ++t) {
+        out.k.push_back(items[t].k);
+        out.len.push_back(items[t].len);
+        out.leaf.push_back(items[t].leaf);
+        for (int l = 0; l < d - 1; ++l) out.pre[static_cast<size_t>(l) * out.n + t] = items[t].pre[static_cast<size_t>(l)];
+    }
+    return out;
+}
+
 // The series program on the device (tiles + group words).
 struct DevProgram {
     DevBuf<int4> tiles;
@@ -491,7 +536,8 @@ struct qrmc_gpu_plan {
     int lanes_per_rank = kLanes;
     DevBuf<uint32_t> d_tile_prog;
     DevBuf<int4> d_tiles;
-    DevBuf<int32_t> d_rows, d_pack_pos;
+    DevBuf<int32_t> d_pack_pos, d_item_k, d_item_len, d_item_leaf, d_item_pre;
+    int n_items = 0;
     DevBuf<double> d_pack_scale, d_alpha, d_coef, d_partials, d_resp, d_cloud;
     DevBuf<unsigned long long> d_counters;
     DevBuf<int> d_flags;
@@ -613,8 +659,6 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     P->d_tiles.upload(pg.tiles.data(), pg.tiles.size(), st);
     P->d_tile_prog.alloc(pg.tile_prog.size());
     P->d_tile_prog.upload(pg.tile_prog.data(), pg.tile_prog.size(), st);
-    P->d_rows.alloc(P->gamma.rows.size());
-    P->d_rows.upload(P->gamma.rows.data(), P->gamma.rows.size(), st);
     P->d_pack_pos.alloc(pg.pack_pos.size());
     P->d_pack_pos.upload(pg.pack_pos.data(), pg.pack_pos.size(), st);
     P->d_pack_scale.alloc(pg.pack_scale.size());
@@ -653,7 +697,6 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     a.abort_flag = P->d_flags.p;
 
     ProjArgs& pa = P->proj;
-    pa.rows = P->d_rows.p;
     int off = 0;
     for (int l = 0; l < d; ++l) {
         pa.offset[l] = off;
@@ -661,6 +704,21 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
         off += P->gamma.kmax[l] + 1;
     }
     pa.table_len = off;
+    const ProjectItems items = build_project_items(P->gamma, pa.offset);
+    P->n_items = items.n;
+    P->d_item_k.alloc(items.k.size());
+    P->d_item_k.upload(items.k.data(), items.k.size(), st);
+    P->d_item_len.alloc(items.len.size());
+    P->d_item_len.upload(items.len.data(), items.len.size(), st);
+    P->d_item_leaf.alloc(items.leaf.size());
+    P->d_item_leaf.upload(items.leaf.data(), items.leaf.size(), st);
+    P->d_item_pre.alloc(items.pre.size());
+    P->d_item_pre.upload(items.pre.data(), items.pre.size(), st);
+    pa.item_k = P->d_item_k.p;
+    pa.item_len = P->d_item_len.p;
+    pa.item_leaf = P->d_item_leaf.p;
+    pa.item_pre = P->d_item_pre.p;
+    pa.n_items = items.n;
     const size_t budget = 96 * 1024;
     const size_t per_point = (static_cast<size_t>(off) + 1) * sizeof(double);
     if (per_point > budget)
@@ -673,7 +731,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     P->ev.resize(3 * static_cast<size_t>(cfg.steps) + 1);
     for (auto& e : P->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     P->launches_per_run = 3 * cfg.steps;
-    P->h2d_bytes = P->gamma.rows.size() * sizeof(int32_t) +
+    P->h2d_bytes = (items.k.size() * 3 + items.pre.size()) * sizeof(int32_t) +
                    pg.pack_pos.size() * sizeof(int32_t) + pg.pack_scale.size() * sizeof(double) +
                    pg.tiles.size() * sizeof(int4) + pg.tile_prog.size() * sizeof(uint32_t);
     P->d2h_bytes = static_cast<uint64_t>(cfg.steps) * P->K * sizeof(double) + 2 * sizeof(unsigned long long) +

@@ -183,12 +183,17 @@ __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
 }
 
 // ---------------------------------------------------------------- K2
-// CTA (term tile, owned lane). Each thread owns kTermsPerThread terms and sums
-// S_m * phi_k(X_m) over the lane's paths in ascending m -- the reference's
-// per-lane order -- with the reference's own table values and product order
-// (cosine_basis.cpp:71-97), so the lane partial is the reference's bit pattern
-// whenever S_m and the cosine values agree.
+// CTA (item tile, owned lane). A work item is a chunk of <= kProjRun leaf
+// indices of one leaf run (host.cpp build_project_items; items sorted by
+// length so a warp's lanes stay in step). Each thread owns kProjItems items
+// and sums S_m * phi_k(X_m) over the lane's paths in ascending m -- the
+// reference's per-lane order -- with the reference's own table values and
+// product order ((1*T_0[k_0])*T_1[k_1])*... (cosine_basis.cpp:71-97), so each
+// lane partial is the reference's bit pattern whenever S_m and the cosine
+// values agree. The run prefix ((T_0*T_1)*...*T_{d-2}) is formed once per
+// (item, point) and shared by the item's terms.
 constexpr int kProjThreads = 256;
+constexpr int kProjItems = 2;
 
 template <int D>
 __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, const ProjArgs p) {
@@ -197,18 +202,21 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, cons
     double* sv = smem + p.batch * p.table_len;   // [batch]
     const int lane_rel = blockIdx.y;
     const int lane = a.lane_lo + lane_rel;
-    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kProjThreads * kTermsPerThread;
+    constexpr int NPRE = D > 1 ? D - 1 : 1;
 
-    int idx[kTermsPerThread][D];
-    bool live[kTermsPerThread];
-    double acc[kTermsPerThread];
+    int pre[kProjItems][NPRE], leaf[kProjItems], len[kProjItems], kfirst[kProjItems];
+    double acc[kProjItems][kProjRun];
 #pragma unroll
-    for (int t = 0; t < kTermsPerThread; ++t) {
-        const int64_t k = k0 + t * kProjThreads + threadIdx.x;
-        live[t] = k < p.basis_size;
-        acc[t] = 0.0;
+    for (int t = 0; t < kProjItems; ++t) {
+        const int it = (blockIdx.x * kProjItems + t) * kProjThreads + threadIdx.x;
+        const bool live = it < p.n_items;
+        len[t] = live ? p.item_len[it] : 0;
+        kfirst[t] = live ? p.item_k[it] : 0;
+        leaf[t] = live ? p.item_leaf[it] : 0;
 #pragma unroll
-        for (int l = 0; l < D; ++l) idx[t][l] = live[t] ? p.offset[l] + p.rows[k * D + l] : 0;
+        for (int l = 0; l < NPRE; ++l) pre[t][l] = (live && D > 1) ? p.item_pre[l * p.n_items + it] : 0;
+#pragma unroll
+        for (int b = 0; b < kProjRun; ++b) acc[t][b] = 0.0;
     }
 
     const int64_t chunks_total = (a.paths + kChunk - 1) / kChunk;
@@ -217,11 +225,11 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, cons
         const int64_t q_chunk = (r * a.owned_lanes + lane_rel) * kChunk;  // owned index of the chunk
         const int64_t m_chunk = c * kChunk;
         const int64_t rem = a.paths - m_chunk;
-        const int len = static_cast<int>(rem < kChunk ? rem : kChunk);
-        for (int base = 0; base < len; base += p.batch) {
-            const int nb = min(p.batch, len - base);
+        const int nlen = static_cast<int>(rem < kChunk ? rem : kChunk);
+        for (int base = 0; base < nlen; base += p.batch) {
+            const int nb = min(p.batch, nlen - base);
             __syncthreads();
-            // tables: one (point, coordinate) recurrence per thread
+            // tables: one (point, coordinate) recurrence per thread (cosine_basis.cpp:67-89)
             for (int task = threadIdx.x; task < nb * D; task += kProjThreads) {
                 const int pt = task / D, l = task % D;
                 const int64_t q = q_chunk + base + pt;
@@ -258,19 +266,26 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, cons
                 const double* t = tab + pt * p.table_len;
                 const double s_m = sv[pt];
 #pragma unroll
-                for (int tt = 0; tt < kTermsPerThread; ++tt) {
-                    double prod = 1.0;
+                for (int it = 0; it < kProjItems; ++it) {
+                    double prefix = 1.0;
+                    if constexpr (D > 1) {
+                        prefix = t[pre[it][0]];
 #pragma unroll
-                    for (int l = 0; l < D; ++l) prod = DMUL(prod, t[idx[tt][l]]);
-                    acc[tt] = DADD(acc[tt], DMUL(s_m, prod));
+                        for (int l = 1; l < D - 1; ++l) prefix = DMUL(prefix, t[pre[it][l]]);
+                    }
+#pragma unroll
+                    for (int b = 0; b < kProjRun; ++b)
+                        if (b < len[it]) acc[it][b] = DADD(acc[it][b], DMUL(s_m, DMUL(prefix, t[leaf[it] + b])));
                 }
             }
         }
     }
 #pragma unroll
-    for (int t = 0; t < kTermsPerThread; ++t) {
-        const int64_t k = k0 + t * kProjThreads + threadIdx.x;
-        if (live[t]) p.partials[static_cast<int64_t>(lane_rel) * p.basis_size + k] = acc[t];
+    for (int it = 0; it < kProjItems; ++it) {
+        double* out = p.partials + static_cast<int64_t>(lane_rel) * p.basis_size + kfirst[it];
+#pragma unroll
+        for (int b = 0; b < kProjRun; ++b)
+            if (b < len[it]) out[b] = acc[it][b];
     }
 }
 
@@ -433,8 +448,8 @@ size_t project_smem_bytes(const ProjArgs& p) {
 }
 
 cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st) {
-    const unsigned tiles = static_cast<unsigned>((p.basis_size + kProjThreads * kTermsPerThread - 1) /
-                                                 (kProjThreads * kTermsPerThread));
+    const unsigned tiles = static_cast<unsigned>((p.n_items + kProjThreads * kProjItems - 1) /
+                                                 (kProjThreads * kProjItems));
     const dim3 grid(tiles, static_cast<unsigned>(a.owned_lanes));
     const size_t smem = project_smem_bytes(p);
     QRMC_DISPATCH_D(a.prob.dim, (k_project<D><<<grid, kProjThreads, smem, st>>>(a, p)));

@@ -10,7 +10,7 @@
 
 namespace qrmc_dev {
 
-constexpr int kTermsPerThread = 2;
+constexpr int kProjRun = 8;  // leaf indices per K2 work item
 
 // Series program in device memory (series_block.cuh).
 struct SeriesTiles {
@@ -43,7 +43,13 @@ struct StepArgs {
 };
 
 struct ProjArgs {
-    const int32_t* rows;  // [K][dim] Gamma rows
+    // work items (host.cpp build_project_items): <= kProjRun consecutive leaf
+    // indices of one run, sorted by length
+    const int32_t* item_k;     // first term index
+    const int32_t* item_len;   // number of terms
+    const int32_t* item_leaf;  // table offset of the first leaf value
+    const int32_t* item_pre;   // [dim-1][n_items] table offsets of the run prefix
+    int n_items;
     int offset[kMaxDim];  // per-coordinate table offsets (cosine_basis.cpp:58-64)
     int kmax[kMaxDim];
     int table_len;

@@ -72,6 +72,7 @@ struct SegState {
     double (&g2p)[P];
     double (&g2c)[P];
     double (&acc2)[P];
+    double (&acc2b)[P];  // second accumulator: odd leaf indices (independent FMA chain)
 
     // sibling weight c_{D-2}[s]: shared table below S2, recurrence (in order) above
     __device__ __forceinline__ void weight(int s, double (&ts)[P]) {
@@ -96,18 +97,23 @@ struct SegState {
     __device__ __forceinline__ void run_fixed(const double2* ra, int s, int cnt) {
         constexpr int NP = (R + 1) / 2;
         auto body = [&](const double (&ts)[P]) {
-            double z[P];
+            // even / odd leaf indices in two independent chains (ILP), folded with
+            // two FMAs so no add sits on the critical path
+            double z0[P], z1[P];
 #pragma unroll
             for (int j = 0; j < NP; ++j) {
                 const double2 a = ra[j];
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
-                    z[p] = j == 0 ? a.x * leaf[p][0] : fma(a.x, leaf[p][2 * j], z[p]);
-                    if (2 * j + 1 < R) z[p] = fma(a.y, leaf[p][2 * j + 1], z[p]);
+                    z0[p] = j == 0 ? a.x * leaf[p][0] : fma(a.x, leaf[p][2 * j], z0[p]);
+                    if (2 * j + 1 < R) z1[p] = j == 0 ? a.y * leaf[p][1] : fma(a.y, leaf[p][2 * j + 1], z1[p]);
                 }
             }
 #pragma unroll
-            for (int p = 0; p < P; ++p) acc2[p] = fma(ts[p], z[p], acc2[p]);
+            for (int p = 0; p < P; ++p) {
+                acc2[p] = fma(ts[p], z0[p], acc2[p]);
+                if (R > 1) acc2b[p] = fma(ts[p], z1[p], acc2b[p]);
+            }
             ra += NP;
         };
         int n_tab = S2 - s;
@@ -185,7 +191,7 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
     constexpr int NU = D > 2 ? D - 2 : 1;  // upper levels 0..D-3
     const int tid = threadIdx.x, nt = blockDim.x;
     double utc[P][NU], ucur[P][NU], uprev[P][NU], uacc[P][NU];
-    double leaf[P][LT], tl[P], t2c[P], acc2[P], g2p[P], g2c[P];
+    double leaf[P][LT], tl[P], t2c[P], acc2[P], acc2b[P], g2p[P], g2c[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
 #pragma unroll
@@ -218,6 +224,7 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
 #pragma unroll
         for (int k = 2; k < LT; ++k) leaf[p][k] = fma(tl[p], leaf[p][k - 1], -leaf[p][k - 2]);
         acc2[p] = 0.0;
+        acc2b[p] = 0.0;
     }
     load_tile(sm, 0, st, row, 0);
     cp_async_commit();
@@ -247,7 +254,7 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
                     if (L != kFirstGroup) {
 #pragma unroll
                         for (int p = 0; p < P; ++p) {
-                            uacc[p][D - 3] = fma(ucur[p][D - 3], acc2[p], uacc[p][D - 3]);
+                            uacc[p][D - 3] = fma(ucur[p][D - 3], acc2[p] + acc2b[p], uacc[p][D - 3]);
 #pragma unroll
                             for (int l = D - 4; l >= 0; --l) {
                                 if (l >= L) {
@@ -272,11 +279,12 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     acc2[p] = 0.0;
+                    acc2b[p] = 0.0;
                     g2p[p] = t2s[((S2 - 2) * P + p) * nt + tid];
                     g2c[p] = t2s[((S2 - 1) * P + p) * nt + tid];
                 }
             }
-            SegState<P, S2, LT> ss{leaf, tl, t2c, t2s + tid, nt, g2p, g2c, acc2};
+            SegState<P, S2, LT> ss{leaf, tl, t2c, t2s + tid, nt, g2p, g2c, acc2, acc2b};
             for (int g = 0; g < n_seg; ++g) {
                 const uint32_t w = pw[i++];
                 const double2* ra = pa + (w & 0x3FFu);
@@ -305,12 +313,12 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         if constexpr (D > 2) {
-            uacc[p][D - 3] = fma(ucur[p][D - 3], acc2[p], uacc[p][D - 3]);
+            uacc[p][D - 3] = fma(ucur[p][D - 3], acc2[p] + acc2b[p], uacc[p][D - 3]);
 #pragma unroll
             for (int l = D - 4; l >= 0; --l) uacc[p][l] = fma(ucur[p][l], uacc[p][l + 1], uacc[p][l]);
             y[p] = uacc[p][0];
         } else {
-            y[p] = acc2[p];
+            y[p] = acc2[p] + acc2b[p];
         }
     }
 }
