@@ -186,7 +186,7 @@ struct Program {
     std::vector<uint32_t> tile_prog; // group program, per-tile 16-byte aligned segments
 };
 
-constexpr int kHostTileA = 2048;  // == kTileA in series_block.cuh
+constexpr int kHostTileA = kSeriesTileA;
 constexpr int kHostTileP = 1024;  // == kTileP
 constexpr uint32_t kFirstGroupCode = 15;
 
@@ -266,7 +266,7 @@ Program build_program(const Gamma& g) {
     // 3. tiles (series_block.cuh): per group chunk a header word, then one word
     // per segment of consecutive equal-length runs; runs never split, groups
     // and segments continue across tiles
-    constexpr int kTileW = 1536;  // == kTileW in series_block.cuh
+    constexpr int kTileW = kSeriesTileW;
     int4 cur = make_int4(0, 0, 0, 0);
     int64_t alpha_pos = 0;
     auto close = [&] {

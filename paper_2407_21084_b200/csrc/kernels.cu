@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
 // values agree. The run prefix ((T_0*T_1)*...*T_{d-2}) is formed once per
 // (item, point) and shared by the item's terms.
 constexpr int kProjThreads = 256;
-constexpr int kProjItems = 2;
+constexpr int kProjItems = 4;
 
 template <int D>
 __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, const ProjArgs p) {
@@ -229,9 +229,12 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, cons
         for (int base = 0; base < nlen; base += p.batch) {
             const int nb = min(p.batch, nlen - base);
             __syncthreads();
-            // tables: one (point, coordinate) recurrence per thread (cosine_basis.cpp:67-89)
-            for (int task = threadIdx.x; task < nb * D; task += kProjThreads) {
-                const int pt = task / D, l = task % D;
+            // tables: one (point, coordinate) recurrence per task (cosine_basis.cpp:67-89);
+            // a second task per pair restarts the recurrence at k0 = kmax/2 from directly
+            // evaluated cosines, halving the serial chain the CTA waits on
+            for (int task = threadIdx.x; task < 2 * nb * D; task += kProjThreads) {
+                const int half = task & 1;
+                const int pt = (task >> 1) / D, l = (task >> 1) % D;
                 const int64_t q = q_chunk + base + pt;
                 double xl;
                 if (a.cloud) {
@@ -243,23 +246,36 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, cons
                     for (int ll = 0; ll <= l; ++ll) u = s.next_uniform();
                     xl = measure_inv_cdf(a.meas, u, l);
                 }
-                const double c1 = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xl, l)));
+                const double theta = DMUL(3.14159265358979323846, measure_cdf(a.meas, xl, l));
+                const double c1 = cos(theta);
                 double* t = tab + pt * p.table_len + p.offset[l];
                 const int kmax = p.kmax[l];
-                t[0] = 1.0;
-                if (kmax >= 1) {
-                    const double sqrt2 = 1.4142135623730951;
-                    double prev = 1.0, cur = c1;
-                    t[1] = DMUL(sqrt2, c1);
-                    const double two_c1 = DMUL(2.0, c1);
-                    for (int k = 2; k <= kmax; ++k) {
+                const int k0 = kmax >= 8 ? kmax / 2 : kmax + 1;  // second half [k0, kmax]
+                const double sqrt2 = 1.4142135623730951;
+                const double two_c1 = DMUL(2.0, c1);
+                if (half == 0) {
+                    t[0] = 1.0;
+                    if (kmax >= 1) {
+                        double prev = 1.0, cur = c1;
+                        t[1] = DMUL(sqrt2, c1);
+                        for (int k = 2; k < k0; ++k) {
+                            const double nx = DSUB(DMUL(two_c1, cur), prev);
+                            prev = cur;
+                            cur = nx;
+                            t[k] = DMUL(sqrt2, nx);
+                        }
+                    }
+                    if (l == 0) sv[pt] = a.resp[q];
+                } else if (k0 <= kmax) {
+                    double prev = cos(static_cast<double>(k0 - 1) * theta), cur = cos(static_cast<double>(k0) * theta);
+                    t[k0] = DMUL(sqrt2, cur);
+                    for (int k = k0 + 1; k <= kmax; ++k) {
                         const double nx = DSUB(DMUL(two_c1, cur), prev);
                         prev = cur;
                         cur = nx;
                         t[k] = DMUL(sqrt2, nx);
                     }
                 }
-                if (l == 0) sv[pt] = a.resp[q];
             }
             __syncthreads();
             for (int pt = 0; pt < nb; ++pt) {

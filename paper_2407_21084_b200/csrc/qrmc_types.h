@@ -14,17 +14,28 @@ constexpr int kMaxDim = 8;
 // register-table sizes S2 (level D-2) and LT (leaf level D-1).
 // QRMC_K1_{P,S2,LT}_D4 override the d = 4 shape (tuning builds only).
 #ifndef QRMC_K1_P_D4
-#define QRMC_K1_P_D4 2
+#define QRMC_K1_P_D4 4
 #endif
 #ifndef QRMC_K1_S2_D4
 #define QRMC_K1_S2_D4 8
 #endif
 #ifndef QRMC_K1_LT_D4
-#define QRMC_K1_LT_D4 16
+#define QRMC_K1_LT_D4 8
 #endif
-constexpr int k1_p(int d) { return d == 4 ? QRMC_K1_P_D4 : d <= 2 || d >= 7 ? 1 : 2; }
-constexpr int k1_s2(int d) { return d == 4 ? QRMC_K1_S2_D4 : d <= 1 ? 2 : d == 2 ? 32 : d == 3 ? 16 : 8; }
-constexpr int k1_lt(int d) { return d == 4 ? QRMC_K1_LT_D4 : d <= 2 ? 32 : d <= 3 ? 16 : 8; }
+// Shared-memory tile of the series program (series_block.cuh / host.cpp):
+// coefficients and 32-bit program words per tile, double-buffered.
+#ifndef QRMC_TILE_A
+#define QRMC_TILE_A 1024
+#endif
+#ifndef QRMC_TILE_W
+#define QRMC_TILE_W 768
+#endif
+constexpr int kSeriesTileA = QRMC_TILE_A;
+constexpr int kSeriesTileW = QRMC_TILE_W;
+
+constexpr int k1_p(int d) { return d == 4 ? QRMC_K1_P_D4 : d == 3 ? 4 : d <= 2 || d >= 7 ? 1 : 2; }
+constexpr int k1_s2(int d) { return d == 4 ? QRMC_K1_S2_D4 : d <= 1 ? 2 : d == 2 ? 32 : 8; }
+constexpr int k1_lt(int d) { return d == 4 ? QRMC_K1_LT_D4 : d <= 2 ? 32 : 8; }
 
 // Product Student-t measure for mu in {1, 2} (proj/src/student.cpp:53-106).
 struct MeasureDev {

@@ -32,8 +32,8 @@
 
 namespace qrmc_dev {
 
-constexpr int kTileA = 2048;    // coefficients per shared-memory tile (16 KiB)
-constexpr int kTileW = 1536;    // program words per tile (6 KiB)
+constexpr int kTileA = kSeriesTileA;  // coefficients per shared-memory tile
+constexpr int kTileW = kSeriesTileW;  // program words per tile
 constexpr int kFirstGroup = 15; // transition code of the first group
 
 struct SeriesSmem {
