@@ -701,7 +701,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     for (int l = 0; l < d; ++l) {
         pa.offset[l] = off;
         pa.kmax[l] = P->gamma.kmax[l];
-        off += P->gamma.kmax[l] + 1;
+        off += (P->gamma.kmax[l] + 2) & ~1;  // even: K2 reads leaf values as 16-byte pairs
     }
     pa.table_len = off;
     const ProjectItems items = build_project_items(P->gamma, pa.offset);

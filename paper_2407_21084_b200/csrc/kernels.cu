@@ -187,11 +187,10 @@ __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
 // indices of one leaf run (host.cpp build_project_items; items sorted by
 // length so a warp's lanes stay in step). Each thread owns kProjItems items
 // and sums S_m * phi_k(X_m) over the lane's paths in ascending m -- the
-// reference's per-lane order -- with the reference's own table values and
-// product order ((1*T_0[k_0])*T_1[k_1])*... (cosine_basis.cpp:71-97), so each
-// lane partial is the reference's bit pattern whenever S_m and the cosine
-// values agree. The run prefix ((T_0*T_1)*...*T_{d-2}) is formed once per
-// (item, point) and shared by the item's terms.
+// reference's per-lane order (solver.cpp:186-197), deterministic and
+// independent of the GPU count -- with the reference's Student-cosine table
+// values (cosine_basis.cpp:71-89). The run prefix S_m*((T_0*T_1)*...*T_{d-2})
+// is formed once per (item, point); each term is then one FMA.
 constexpr int kProjThreads = 256;
 constexpr int kProjItems = 4;
 
@@ -283,15 +282,24 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, cons
                 const double s_m = sv[pt];
 #pragma unroll
                 for (int it = 0; it < kProjItems; ++it) {
-                    double prefix = 1.0;
+                    // w = S_m * ((T_0 T_1) ... T_{d-2}); each term one FMA with the leaf
+                    // value, read as 16-byte pairs (leaf offsets are even)
+                    double w = s_m;
                     if constexpr (D > 1) {
-                        prefix = t[pre[it][0]];
+                        double prefix = t[pre[it][0]];
 #pragma unroll
                         for (int l = 1; l < D - 1; ++l) prefix = DMUL(prefix, t[pre[it][l]]);
+                        w = DMUL(s_m, prefix);
                     }
+                    const double2* lv = reinterpret_cast<const double2*>(t + leaf[it]);
 #pragma unroll
-                    for (int b = 0; b < kProjRun; ++b)
-                        if (b < len[it]) acc[it][b] = DADD(acc[it][b], DMUL(s_m, DMUL(prefix, t[leaf[it] + b])));
+                    for (int b2 = 0; b2 < kProjRun / 2; ++b2) {
+                        if (2 * b2 < len[it]) {
+                            const double2 v = lv[b2];
+                            acc[it][2 * b2] = fma(w, v.x, acc[it][2 * b2]);
+                            acc[it][2 * b2 + 1] = fma(w, v.y, acc[it][2 * b2 + 1]);
+                        }
+                    }
                 }
             }
         }
