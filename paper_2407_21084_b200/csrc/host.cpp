@@ -452,6 +452,18 @@ ProjectItems build_project_items(const Gamma& g, const int* offset) {
         i = j;
     }
     std::stable_sort(items.begin(), items.end(), [](const It& a, const It& b) { return a.len > b.len; });
+    // pad every length class to whole warps (32 items) with empty items, so the
+    // kernel's per-warp dispatch on the item length is uniform
+    {
+        std::vector<It> padded;
+        for (size_t i = 0; i < items.size();) {
+            size_t j = i;
+            while (j < items.size() && items[j].len == items[i].len) padded.push_back(items[j++]);
+            while (padded.size() % 32) padded.push_back(It{0, 0, 0, std::vector<int32_t>(static_cast<size_t>(std::max(d - 1, 0)), 0)});
+            i = j;
+        }
+        items.swap(padded);
+    }
     ProjectItems out;
     out.n = static_cast<int>(items.size());
     const int np = std::max(d - 1, 1);

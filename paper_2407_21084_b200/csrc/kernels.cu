@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "qrmc_device.cuh"
@@ -277,29 +278,43 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, cons
                 }
             }
             __syncthreads();
-            for (int pt = 0; pt < nb; ++pt) {
-                const double* t = tab + pt * p.table_len;
-                const double s_m = sv[pt];
 #pragma unroll
-                for (int it = 0; it < kProjItems; ++it) {
-                    // w = S_m * ((T_0 T_1) ... T_{d-2}); each term one FMA with the leaf
-                    // value, read as 16-byte pairs (leaf offsets are even)
-                    double w = s_m;
-                    if constexpr (D > 1) {
-                        double prefix = t[pre[it][0]];
+            for (int it = 0; it < kProjItems; ++it) {
+                // item lengths are uniform per warp (host pads length classes to whole
+                // warps): one dispatch per (item slot, batch) into a static-length loop
+                auto points = [&](auto len_c) {
+                    constexpr int LEN = decltype(len_c)::value;
+                    constexpr int NP2 = (LEN + 1) / 2;
+                    for (int pt = 0; pt < nb; ++pt) {
+                        const double* t = tab + pt * p.table_len;
+                        // w = S_m * ((T_0 T_1) ... T_{d-2}); each term one FMA with the leaf
+                        // value, read as 16-byte pairs (leaf offsets are even)
+                        double w = sv[pt];
+                        if constexpr (D > 1) {
+                            double prefix = t[pre[it][0]];
 #pragma unroll
-                        for (int l = 1; l < D - 1; ++l) prefix = DMUL(prefix, t[pre[it][l]]);
-                        w = DMUL(s_m, prefix);
-                    }
-                    const double2* lv = reinterpret_cast<const double2*>(t + leaf[it]);
+                            for (int l = 1; l < D - 1; ++l) prefix = DMUL(prefix, t[pre[it][l]]);
+                            w = DMUL(w, prefix);
+                        }
+                        const double2* lv = reinterpret_cast<const double2*>(t + leaf[it]);
 #pragma unroll
-                    for (int b2 = 0; b2 < kProjRun / 2; ++b2) {
-                        if (2 * b2 < len[it]) {
+                        for (int b2 = 0; b2 < NP2; ++b2) {
                             const double2 v = lv[b2];
                             acc[it][2 * b2] = fma(w, v.x, acc[it][2 * b2]);
-                            acc[it][2 * b2 + 1] = fma(w, v.y, acc[it][2 * b2 + 1]);
+                            if (2 * b2 + 1 < LEN) acc[it][2 * b2 + 1] = fma(w, v.y, acc[it][2 * b2 + 1]);
                         }
                     }
+                };
+                switch (len[it]) {
+                    case 1: points(std::integral_constant<int, 1>{}); break;
+                    case 2: points(std::integral_constant<int, 2>{}); break;
+                    case 3: points(std::integral_constant<int, 3>{}); break;
+                    case 4: points(std::integral_constant<int, 4>{}); break;
+                    case 5: points(std::integral_constant<int, 5>{}); break;
+                    case 6: points(std::integral_constant<int, 6>{}); break;
+                    case 7: points(std::integral_constant<int, 7>{}); break;
+                    case 8: points(std::integral_constant<int, 8>{}); break;
+                    default: break;
                 }
             }
         }
