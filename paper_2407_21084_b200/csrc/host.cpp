@@ -731,7 +731,10 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     pa.item_leaf = P->d_item_leaf.p;
     pa.item_pre = P->d_item_pre.p;
     pa.n_items = items.n;
-    const size_t budget = 96 * 1024;
+#ifndef QRMC_PROJ_SMEM_KB
+#define QRMC_PROJ_SMEM_KB 96
+#endif
+    const size_t budget = QRMC_PROJ_SMEM_KB * 1024;  // K2 point-table staging
     const size_t per_point = (static_cast<size_t>(off) + 1) * sizeof(double);
     if (per_point > budget)
         fail(QRMC_ENOTIMPL, fmt("per-point basis table of %d entries exceeds shared memory", off));

@@ -192,8 +192,14 @@ __global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
 // independent of the GPU count -- with the reference's Student-cosine table
 // values (cosine_basis.cpp:71-89). The run prefix S_m*((T_0*T_1)*...*T_{d-2})
 // is formed once per (item, point); each term is then one FMA.
-constexpr int kProjThreads = 256;
-constexpr int kProjItems = 4;
+#ifndef QRMC_PROJ_THREADS
+#define QRMC_PROJ_THREADS 256
+#endif
+constexpr int kProjThreads = QRMC_PROJ_THREADS;
+#ifndef QRMC_PROJ_ITEMS
+#define QRMC_PROJ_ITEMS 4
+#endif
+constexpr int kProjItems = QRMC_PROJ_ITEMS;  // items per thread
 
 template <int D>
 __global__ void __launch_bounds__(kProjThreads) k_project(const StepArgs a, const ProjArgs p) {
