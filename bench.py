@@ -43,6 +43,18 @@ METRIC = "simulated paths x time-steps per second per full backward solve"
 UNIT = "path-steps/s"
 
 
+def traffic_per_launch():
+    """DRAM bytes (read + write) per k_responses launch from the committed ncu
+    --set full capture of this workload (profiles/roofline_traffic.json), or None."""
+    f = ROOT / "profiles" / "roofline_traffic.json"
+    if not f.exists():
+        return None
+    try:
+        return json.loads(f.read_text())["k_responses"]["dram_bytes_per_launch"]
+    except (KeyError, ValueError):
+        return None
+
+
 def peaks() -> dict:
     p = {}
     f = ROOT / "MEASURED_PEAKS.json"
@@ -307,7 +319,7 @@ def run_ours(args) -> int:
                                          "k_finish_step": kernel_s[2] / args.steps},
             "roofline": {"kernel": "k_responses", "bound": "fp64", "achieved": achieved,
                          "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"],
-                         "traffic": None,
+                         "traffic": traffic_per_launch(),
                          "peak_source": "measured FP64 (DMMA 37.1 TF/s) on this pool, profiles/r01_fp64_peak.txt"},
             "e2e": {"value": path_steps(paths_total, n) / e2e_t, "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value)},

@@ -69,7 +69,10 @@ constexpr size_t series_smem_bytes(int P, bool paths = false) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kK1Threads) k_responses(const StepArgs a) {
+#ifndef QRMC_K1_MIN_BLOCKS
+#define QRMC_K1_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kK1Threads, QRMC_K1_MIN_BLOCKS) k_responses(const StepArgs a) {
     constexpr int P = k1_p(D), S2 = k1_s2(D), LT = k1_lt(D);
     extern __shared__ __align__(16) unsigned char dsm[];
     SeriesSmem& sm = *reinterpret_cast<SeriesSmem*>(dsm);
