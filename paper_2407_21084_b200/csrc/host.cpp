@@ -277,6 +277,29 @@ Program build_program(const Gamma& g) {
     auto open = [&] { cur = make_int4(static_cast<int>(p.tile_prog.size()), 0, static_cast<int>(alpha_pos), 0); };
     open();
     for (const Group& gr : groups) {
+        // hyperbolic-profile group (R_s = floor(B / max(s,1)) + 1, s = 0..B) small
+        // enough for the static code of series_block.cuh: header + {pair offset, B}
+        {
+            const int B = static_cast<int>(gr.n) - 1;
+            bool hyp = d >= 2 && B >= 1 && B <= 7 && B + 1 <= k1_s2(d) && B + 1 <= k1_lt(d);
+            int64_t total = 0;
+            for (size_t q = 0; hyp && q < gr.n; ++q) {
+                hyp = runs[gr.r0 + q].R == B / static_cast<int64_t>(std::max<size_t>(q, 1)) + 1;
+                total += (runs[gr.r0 + q].R + 1) & ~int64_t{1};
+            }
+            if (hyp) {
+                if (cur.w + total > kHostTileA || cur.y + 2 > kTileW) {
+                    close();
+                    open();
+                }
+                p.tile_prog.push_back(gr.L << 12 | (1u << 29));
+                p.tile_prog.push_back(static_cast<uint32_t>(cur.w / 2) | (static_cast<uint32_t>(B) << 16));
+                cur.y += 2;
+                cur.w += static_cast<int>(total);
+                alpha_pos += total;
+                continue;
+            }
+        }
         size_t s = 0;
         while (s < gr.n) {
             const int64_t R0 = runs[gr.r0 + s].R;
