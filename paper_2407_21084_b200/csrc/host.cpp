@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -281,7 +282,8 @@ Program build_program(const Gamma& g) {
         // enough for the static code of series_block.cuh: header + {pair offset, B}
         {
             const int B = static_cast<int>(gr.n) - 1;
-            bool hyp = d >= 2 && B >= 1 && B <= 7 && B + 1 <= k1_s2(d) && B + 1 <= k1_lt(d);
+            // mirrors hyp_supported (series_block.cuh)
+            bool hyp = d >= 2 && B >= 1 && B <= kHypMaxB && k1_lt(d) >= 2 && k1_s2(d) >= 2;
             int64_t total = 0;
             for (size_t q = 0; hyp && q < gr.n; ++q) {
                 hyp = runs[gr.r0 + q].R == B / static_cast<int64_t>(std::max<size_t>(q, 1)) + 1;
@@ -500,6 +502,147 @@ ProjectItems build_project_items(const Gamma& g, const int* offset) {
     return out;
 }
 
+// Fragment-stream layout of the tensor-core K1 (responses_mma.cu). Groups are
+// the upper prefixes u = (k_0..k_{d-3}); each holds a set of (s, b) =
+// (k_{d-2}, k_{d-1}) pairs. Pairs are ordered by how many groups contain them
+// (then lexicographically); for a chain of sets (full, total-degree and
+// hyperbolic index sets) every group is then a prefix of that order, which is
+// checked here -- ok = false sends the plan to the series-program K1.
+struct MmaLayout {
+    bool ok = false;
+    std::vector<uint32_t> terms;    // [n_terms] table offsets (s | b << 16)
+    std::vector<uint16_t> gk;       // [n_groups][d-2] table offsets of the prefix
+    std::vector<int4> units;        // {cb0, nb, c0, c1}, warp-contiguous
+    std::vector<int4> warp_info;    // [kMmaWarps] {unit_begin, unit_end, frag_offset, frags}
+    std::vector<int32_t> pos;       // k -> position in the per-series stream
+    int64_t row_len = 0;
+    int64_t frags = 0;              // B fragments per series (useful MACs = K of 256 * frags)
+};
+
+MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
+    MmaLayout L;
+    const int d = g.dim;
+    const int64_t K = g.size();
+    if (d < 3 || K == 0) return L;
+    const int nu = d - 2;
+    auto at = [&](int64_t r, int l) { return g.rows[static_cast<size_t>(r * d + l)]; };
+    // groups: maximal runs of rows with equal prefix (rows are lexicographic)
+    struct Grp { int64_t r0, n; };
+    std::vector<Grp> groups;
+    for (int64_t r = 0; r < K;) {
+        int64_t e = r + 1;
+        auto same = [&](int64_t q) {
+            for (int l = 0; l < nu; ++l)
+                if (at(q, l) != at(r, l)) return false;
+            return true;
+        };
+        while (e < K && same(e)) ++e;
+        groups.push_back({r, e - r});
+        r = e;
+    }
+    const int S = g.kmax[d - 2] + 1, Bn = g.kmax[d - 1] + 1;
+    std::vector<int32_t> cnt(static_cast<size_t>(S) * Bn, 0);
+    for (int64_t r = 0; r < K; ++r) ++cnt[static_cast<size_t>(at(r, d - 2)) * Bn + at(r, d - 1)];
+    std::vector<int32_t> order;
+    for (int32_t pr = 0; pr < S * Bn; ++pr)
+        if (cnt[static_cast<size_t>(pr)]) order.push_back(pr);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t x, int32_t y) { return cnt[static_cast<size_t>(x)] > cnt[static_cast<size_t>(y)]; });
+    std::vector<int32_t> rank(static_cast<size_t>(S) * Bn, -1);
+    for (size_t t = 0; t < order.size(); ++t) rank[static_cast<size_t>(order[t])] = static_cast<int32_t>(t);
+    for (const Grp& gr : groups)
+        for (int64_t r = gr.r0; r < gr.r0 + gr.n; ++r)
+            if (rank[static_cast<size_t>(at(r, d - 2)) * Bn + at(r, d - 1)] >= gr.n) return L;  // not a prefix
+    if (static_cast<int64_t>(offset[d - 1] + Bn) * kMmaTabStride > 0xFFFF) return L;
+    auto row_of = [](int entry) { return static_cast<uint32_t>(entry * kMmaTabStride); };
+    const int n_terms = static_cast<int>((order.size() + 3) & ~size_t{3});
+    L.terms.assign(static_cast<size_t>(n_terms), row_of(offset[d - 2]) | row_of(offset[d - 1]) << 16);
+    for (size_t t = 0; t < order.size(); ++t)
+        L.terms[t] = row_of(offset[d - 2] + order[t] / Bn) | row_of(offset[d - 1] + order[t] % Bn) << 16;
+
+    // groups by size (descending, stable), 8 per column block
+    std::vector<int32_t> gi(groups.size());
+    for (size_t i = 0; i < gi.size(); ++i) gi[i] = static_cast<int32_t>(i);
+    std::stable_sort(gi.begin(), gi.end(), [&](int32_t x, int32_t y) { return groups[x].n > groups[y].n; });
+    const int n_cb = static_cast<int>((gi.size() + 7) / 8);
+    L.gk.assign(static_cast<size_t>(n_cb) * 8 * nu, 0);
+    for (int c = 0; c < n_cb * 8; ++c)
+        for (int l = 0; l < nu; ++l)
+            L.gk[static_cast<size_t>(c) * nu + l] = static_cast<uint16_t>(
+                row_of(offset[l] + (c < static_cast<int>(gi.size()) ? at(groups[gi[c]].r0, l) : 0)));
+    std::vector<int32_t> cb_chunks;  // chunks of 4 terms per column block (descending)
+    for (int cb = 0; cb < n_cb; ++cb) cb_chunks.push_back(static_cast<int32_t>((groups[gi[8 * cb]].n + 3) / 4));
+
+    // units: column blocks of equal chunk count, <= kMmaBundle per unit, chunk
+    // range cut into <= kMmaKSplit pieces; balanced over the warps (longest
+    // processing time first) with an issue-slot cost model
+    struct Unit { int cb0, nb, c0, c1; double cost; };
+    std::vector<Unit> units;
+    for (int cb = 0; cb < n_cb;) {
+        int e = cb;
+        while (e < n_cb && e - cb < kMmaBundle && cb_chunks[e] == cb_chunks[cb]) ++e;
+        const int E = cb_chunks[cb], nb = e - cb;
+        const int np = (E + kMmaKSplit - 1) / kMmaKSplit;
+        for (int q = 0; q < np; ++q) {
+            const int c0 = static_cast<int>(static_cast<int64_t>(E) * q / np);
+            const int c1 = static_cast<int>(static_cast<int64_t>(E) * (q + 1) / np);
+            const double len = c1 - c0;
+            units.push_back({cb, nb, c0, c1, len * (16.0 + nb * 10.0) + nb * 48.0});
+        }
+        cb = e;
+    }
+    std::vector<int32_t> ui(units.size());
+    for (size_t i = 0; i < ui.size(); ++i) ui[i] = static_cast<int32_t>(i);
+    std::stable_sort(ui.begin(), ui.end(), [&](int32_t x, int32_t y) { return units[x].cost > units[y].cost; });
+    std::vector<std::vector<int32_t>> per_warp(kMmaWarps);
+    std::vector<double> load(kMmaWarps, 0.0);
+    for (int32_t u : ui) {
+        const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        per_warp[w].push_back(u);
+        load[w] += units[u].cost;
+    }
+    std::vector<int64_t> frag_at(static_cast<size_t>(n_cb) * cb_chunks[0], -1);
+    const int cstride = cb_chunks[0];
+    int64_t woff = 0;
+    for (int w = 0; w < kMmaWarps; ++w) {
+        std::sort(per_warp[w].begin(), per_warp[w].end(), [&](int32_t x, int32_t y) {
+            return units[x].cb0 != units[y].cb0 ? units[x].cb0 < units[y].cb0 : units[x].c0 < units[y].c0;
+        });
+        const int ub = static_cast<int>(L.units.size());
+        int64_t f = 0;
+        for (int32_t u : per_warp[w]) {
+            const Unit& un = units[u];
+            L.units.push_back(make_int4(un.cb0, un.nb, un.c0, un.c1));
+            // a step takes 1, 2 or 4 fragment slots (3 column blocks use 4), aligned,
+            // so no step straddles the ring wrap
+            const int stride = un.nb == 3 ? 4 : un.nb;
+            f = (f + stride - 1) / stride * stride;
+            for (int c = un.c0; c < un.c1; ++c, f += stride)
+                for (int i = 0; i < un.nb; ++i) frag_at[static_cast<size_t>(un.cb0 + i) * cstride + c] = woff + f + i;
+        }
+        L.frags += f;
+        const int64_t fpad = (f + kMmaRingFrags - 1) / kMmaRingFrags * kMmaRingFrags;
+        L.warp_info.push_back(make_int4(ub, static_cast<int>(L.units.size()), static_cast<int>(woff), static_cast<int>(fpad)));
+        woff += fpad;
+    }
+    L.row_len = woff * 32;
+    if (L.row_len >= (int64_t{1} << 31)) return MmaLayout{};
+    // k -> stream position: column n of block cb, term t in chunk t/4 row t%4
+    L.pos.assign(static_cast<size_t>(K), 0);
+    for (int c = 0; c < static_cast<int>(gi.size()); ++c) {
+        const Grp& gr = groups[gi[c]];
+        const int cb = c / 8, n = c % 8;
+        for (int64_t r = gr.r0; r < gr.r0 + gr.n; ++r) {
+            const int t = rank[static_cast<size_t>(at(r, d - 2)) * Bn + at(r, d - 1)];
+            const int64_t f = frag_at[static_cast<size_t>(cb) * cstride + t / 4];
+            if (f < 0) fail(QRMC_ELOGIC, "mma layout: term outside the fragment stream");
+            L.pos[static_cast<size_t>(r)] = static_cast<int32_t>(f * 32 + ((n << 2) | (t & 3)));
+        }
+    }
+    L.ok = true;
+    return L;
+}
+
 // The series program on the device (tiles + group words).
 struct DevProgram {
     DevBuf<int4> tiles;
@@ -573,6 +716,14 @@ struct qrmc_gpu_plan {
     DevBuf<int4> d_tiles;
     DevBuf<int32_t> d_pack_pos, d_item_k, d_item_len, d_item_leaf, d_item_pre;
     int n_items = 0;
+    // tensor-core K1 (responses_mma.cu), when the index set allows it
+    bool use_mma = false;
+    MmaArgs mma{};
+    DevBuf<double> d_alpha_mma;
+    DevBuf<int4> d_mma_units, d_mma_warps;
+    DevBuf<uint32_t> d_mma_terms;
+    DevBuf<uint16_t> d_mma_gk;
+    DevBuf<int32_t> d_mma_pos;
     DevBuf<double> d_pack_scale, d_alpha, d_coef, d_partials, d_resp, d_cloud;
     DevBuf<unsigned long long> d_counters;
     DevBuf<int> d_flags;
@@ -639,7 +790,10 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
     for (int i = N - 1; i >= 0; --i) {
         StepArgs a = P.base;
         a.step = i;
-        cuda_check(launch_responses(a, st), "k_responses");
+        if (P.use_mma)
+            cuda_check(launch_responses_mma(a, P.mma, st), "k_responses_mma");
+        else
+            cuda_check(launch_responses(a, st), "k_responses");
         mark();
         ProjArgs pa = P.proj;
         pa.partials = P.d_partials.p + static_cast<size_t>(P.session->rank) * P.lanes_per_rank * P.K;
@@ -657,6 +811,11 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
         f.coef_row = P.d_coef.p + static_cast<size_t>(i) * P.K;
         f.pack_pos = P.d_pack_pos.p;
         f.pack_scale = P.d_pack_scale.p;
+        if (P.use_mma) {
+            f.alpha_mma = P.d_alpha_mma.p;
+            f.mma_row_len = P.mma.row_len;
+            f.mma_pos = P.d_mma_pos.p;
+        }
         cuda_check(launch_finish(a, f, st), "k_finish_step");
         mark();
     }
@@ -764,12 +923,55 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     pa.batch = static_cast<int>(std::min<size_t>(64, budget / per_point));
     pa.basis_size = P->K;
 
+    // tensor-core K1 when the index set is a chain of (s, b) prefixes and the
+    // per-path tables fit shared memory; QRMC_K1=series forces the series program
+    {
+        const char* k1 = std::getenv("QRMC_K1");
+        const bool want = !(k1 && std::strcmp(k1, "series") == 0);
+        const size_t smem = responses_mma_smem_bytes(d, off);
+        int optin = 0;
+        cuda_check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device), "attr");
+        if (want && d >= 3 && smem && smem <= static_cast<size_t>(optin)) {
+            MmaLayout L = build_mma_layout(P->gamma, pa.offset);
+            if (L.ok) {
+                P->use_mma = true;
+                P->d_mma_units.alloc(L.units.size());
+                P->d_mma_units.upload(L.units.data(), L.units.size(), st);
+                P->d_mma_warps.alloc(L.warp_info.size());
+                P->d_mma_warps.upload(L.warp_info.data(), L.warp_info.size(), st);
+                P->d_mma_terms.alloc(L.terms.size());
+                P->d_mma_terms.upload(L.terms.data(), L.terms.size(), st);
+                P->d_mma_gk.alloc(L.gk.size());
+                P->d_mma_gk.upload(L.gk.data(), L.gk.size(), st);
+                P->d_mma_pos.alloc(L.pos.size());
+                P->d_mma_pos.upload(L.pos.data(), L.pos.size(), st);
+                P->d_alpha_mma.alloc(static_cast<size_t>(cfg.steps) * L.row_len);
+                cuda_check(cudaMemsetAsync(P->d_alpha_mma.p, 0, P->d_alpha_mma.n * sizeof(double), st), "memset");
+                MmaArgs& m = P->mma;
+                m.alpha = P->d_alpha_mma.p;
+                m.row_len = L.row_len;
+                m.units = P->d_mma_units.p;
+                m.warp_info = P->d_mma_warps.p;
+                m.terms = P->d_mma_terms.p;
+                m.gk = P->d_mma_gk.p;
+                m.table_len = off;
+                for (int l = 0; l < d; ++l) {
+                    m.offset[l] = pa.offset[l];
+                    m.kmax[l] = pa.kmax[l];
+                }
+                cuda_check(configure_responses_mma(d, smem), "k_responses_mma attributes");
+                P->h2d_bytes += (L.units.size() + L.warp_info.size()) * sizeof(int4) +
+                                L.terms.size() * sizeof(uint32_t) + L.gk.size() * sizeof(uint16_t) +
+                                L.pos.size() * sizeof(int32_t);
+            }
+        }
+    }
     cuda_check(configure_project(d, project_smem_bytes(pa)), "k_project attributes");
     cuda_check(configure_series_kernels(), "series kernel attributes");
     P->ev.resize(3 * static_cast<size_t>(cfg.steps) + 1);
     for (auto& e : P->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     P->launches_per_run = 3 * cfg.steps;
-    P->h2d_bytes = (items.k.size() * 3 + items.pre.size()) * sizeof(int32_t) +
+    P->h2d_bytes += (items.k.size() * 3 + items.pre.size()) * sizeof(int32_t) +
                    pg.pack_pos.size() * sizeof(int32_t) + pg.pack_scale.size() * sizeof(double) +
                    pg.tiles.size() * sizeof(int4) + pg.tile_prog.size() * sizeof(uint32_t);
     P->d2h_bytes = static_cast<uint64_t>(cfg.steps) * P->K * sizeof(double) + 2 * sizeof(unsigned long long) +

@@ -346,7 +346,9 @@ __global__ void k_finish_step(const StepArgs a, const FinishArgs f) {
     const double v = DMUL(sum, f.inv_m);
     if (!isfinite(v)) record_error(a.err_flags, QRMC_ENUMERIC, 0);
     f.coef_row[k] = v;
-    a.alpha_packed[static_cast<int64_t>(a.step) * a.kp + f.pack_pos[k]] = DMUL(v, f.pack_scale[k]);
+    const double scaled = DMUL(v, f.pack_scale[k]);
+    a.alpha_packed[static_cast<int64_t>(a.step) * a.kp + f.pack_pos[k]] = scaled;
+    if (f.alpha_mma) f.alpha_mma[static_cast<int64_t>(a.step) * f.mma_row_len + f.mma_pos[k]] = scaled;
 }
 
 // ---------------------------------------------------------------- probes
@@ -448,17 +450,53 @@ __global__ void __launch_bounds__(kK1Threads) k_mse(const StepArgs a, double kap
 }
 
 // ---------------------------------------------------------------- dispatch
-#define QRMC_DISPATCH_D(dim, ...)                  \
-    switch (dim) {                                  \
-        case 1: { constexpr int D = 1; __VA_ARGS__; } break; \
-        case 2: { constexpr int D = 2; __VA_ARGS__; } break; \
-        case 3: { constexpr int D = 3; __VA_ARGS__; } break; \
-        case 4: { constexpr int D = 4; __VA_ARGS__; } break; \
-        case 5: { constexpr int D = 5; __VA_ARGS__; } break; \
-        case 6: { constexpr int D = 6; __VA_ARGS__; } break; \
-        case 7: { constexpr int D = 7; __VA_ARGS__; } break; \
-        case 8: { constexpr int D = 8; __VA_ARGS__; } break; \
-        default: return cudaErrorInvalidValue;      \
+// QRMC_ONLY_DIM=n (tuning builds only) instantiates the kernels for D = n alone.
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 1
+#define QRMC_DCASE1(...) case 1: { constexpr int D = 1; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE1(...)
+#endif
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 2
+#define QRMC_DCASE2(...) case 2: { constexpr int D = 2; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE2(...)
+#endif
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 3
+#define QRMC_DCASE3(...) case 3: { constexpr int D = 3; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE3(...)
+#endif
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 4
+#define QRMC_DCASE4(...) case 4: { constexpr int D = 4; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE4(...)
+#endif
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 5
+#define QRMC_DCASE5(...) case 5: { constexpr int D = 5; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE5(...)
+#endif
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 6
+#define QRMC_DCASE6(...) case 6: { constexpr int D = 6; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE6(...)
+#endif
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 7
+#define QRMC_DCASE7(...) case 7: { constexpr int D = 7; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE7(...)
+#endif
+#if !defined(QRMC_ONLY_DIM) || QRMC_ONLY_DIM == 8
+#define QRMC_DCASE8(...) case 8: { constexpr int D = 8; __VA_ARGS__; } break;
+#else
+#define QRMC_DCASE8(...)
+#endif
+#define QRMC_DISPATCH_D(dim, ...)                                                     \
+    switch (dim) {                                                                     \
+        QRMC_DCASE1(__VA_ARGS__) QRMC_DCASE2(__VA_ARGS__) QRMC_DCASE3(__VA_ARGS__)     \
+        QRMC_DCASE4(__VA_ARGS__) QRMC_DCASE5(__VA_ARGS__) QRMC_DCASE6(__VA_ARGS__)     \
+        QRMC_DCASE7(__VA_ARGS__) QRMC_DCASE8(__VA_ARGS__)                              \
+        default: return cudaErrorInvalidValue;                                         \
     }
 
 // Opt every series kernel into > 48 KiB of dynamic shared memory (once per process).
@@ -473,8 +511,12 @@ cudaError_t configure_series_kernels() {
     set(reinterpret_cast<const void*>(&k_responses<Dv>), series_smem_bytes<Dv>(k1_p(Dv), true));          \
     set(reinterpret_cast<const void*>(&k_eval_points<Dv>), series_smem_bytes<Dv>(1));              \
     set(reinterpret_cast<const void*>(&k_mse<Dv>), series_smem_bytes<Dv>(1));
+#ifdef QRMC_ONLY_DIM
+        QRMC_CONFIGURE(QRMC_ONLY_DIM)
+#else
         QRMC_CONFIGURE(1) QRMC_CONFIGURE(2) QRMC_CONFIGURE(3) QRMC_CONFIGURE(4)
         QRMC_CONFIGURE(5) QRMC_CONFIGURE(6) QRMC_CONFIGURE(7) QRMC_CONFIGURE(8)
+#endif
 #undef QRMC_CONFIGURE
         return e;
     }();

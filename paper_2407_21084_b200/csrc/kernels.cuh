@@ -42,6 +42,38 @@ struct StepArgs {
     const int* abort_flag;
 };
 
+// K1 on the FP64 tensor cores (responses_mma.cu, host.cpp build_mma_layout).
+// The CTA owns 8*kMmaRowBlocks paths; every warp runs mma.m8n8k4.f64 for all of
+// them on its own units (column blocks x chunk range), streaming its own
+// coefficient fragments through a private shared-memory ring.
+#ifndef QRMC_MMA_WARPS
+#define QRMC_MMA_WARPS 8
+#endif
+constexpr int kMmaWarps = QRMC_MMA_WARPS;
+constexpr int kMmaRowBlocks = 4;                 // 8-path row blocks per CTA
+constexpr int kMmaPaths = 8 * kMmaRowBlocks;     // paths per CTA
+constexpr int kMmaBundle = 4;                    // max column blocks per unit
+constexpr int kMmaBatch = 8;                     // fragments per copy batch (2 KiB)
+constexpr int kMmaRingBatches = 4;               // per-warp ring depth
+constexpr int kMmaRingFrags = kMmaBatch * kMmaRingBatches;
+constexpr int kMmaTabStride = kMmaPaths + 4;    // cosine tables [table entry][path], padded
+#ifndef QRMC_MMA_KSPLIT
+#define QRMC_MMA_KSPLIT 16
+#endif
+constexpr int kMmaKSplit = QRMC_MMA_KSPLIT;      // max chunks per unit
+
+struct MmaArgs {
+    const double* alpha;      // [N][row_len] fragment streams per series
+    int64_t row_len;          // doubles per series
+    const int4* units;        // {cb0, nb, c0, c1}, warp-contiguous
+    const int4* warp_info;    // [kMmaWarps] {unit_begin, unit_end, frag_offset, frags (padded to kMmaBatch)}
+    const uint32_t* terms;    // [n_terms] table rows (x kMmaTabStride) of c_s(x_{D-2}) | c_b(x_{D-1}) << 16
+    const uint16_t* gk;       // [n_groups][D-2] table rows (x kMmaTabStride) of the group prefix
+    int table_len;            // doubles per path table (all coordinates)
+    int offset[kMaxDim];      // per-coordinate table offsets
+    int kmax[kMaxDim];
+};
+
 struct ProjArgs {
     // work items (host.cpp build_project_items): <= kProjRun consecutive leaf
     // indices of one run, sorted by length
@@ -65,10 +97,16 @@ struct FinishArgs {
     double* coef_row;            // [K] canonical alpha_i
     const int32_t* pack_pos;     // k -> packed position
     const double* pack_scale;    // sqrt2^{nnz(k)}
+    double* alpha_mma;           // [N][mma_row_len] fragment stream, or nullptr
+    int64_t mma_row_len;
+    const int32_t* mma_pos;      // k -> fragment-stream position
 };
 
 cudaError_t configure_series_kernels();  // once per process, before the first series launch
 cudaError_t launch_responses(const StepArgs& a, cudaStream_t st);
+size_t responses_mma_smem_bytes(int dim, int table_len);
+cudaError_t configure_responses_mma(int dim, size_t smem);
+cudaError_t launch_responses_mma(const StepArgs& a, const MmaArgs& m, cudaStream_t st);
 size_t project_smem_bytes(const ProjArgs& p);
 cudaError_t configure_project(int dim, size_t smem);
 cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st);

@@ -33,6 +33,12 @@ constexpr int kMaxDim = 8;
 constexpr int kSeriesTileA = QRMC_TILE_A;
 constexpr int kSeriesTileW = QRMC_TILE_W;
 
+// Largest budget B of the hyperbolic-profile groups run by static code (series_block.cuh).
+#ifndef QRMC_HYP_MAX_B
+#define QRMC_HYP_MAX_B 7
+#endif
+constexpr int kHypMaxB = QRMC_HYP_MAX_B;
+
 constexpr int k1_p(int d) { return d == 4 ? QRMC_K1_P_D4 : d == 3 ? 4 : d <= 2 || d >= 7 ? 1 : 2; }
 constexpr int k1_s2(int d) { return d == 4 ? QRMC_K1_S2_D4 : d <= 1 ? 2 : d == 2 ? 32 : 8; }
 constexpr int k1_lt(int d) { return d == 4 ? QRMC_K1_LT_D4 : d <= 2 ? 32 : 8; }

@@ -1,0 +1,426 @@
+// responses_mma.cu -- K1 (phase 1 of backward step i) on the FP64 tensor cores.
+//
+// Same contract as k_responses in kernels.cu (proj/src/solver.cpp:147-177):
+// per path m, draw X_i ~ nu, Euler to N, evaluate every future series
+// alpha_{j+1} at X_{j+1}, truncate, accumulate the driver, emit S_m.
+//
+// The series sum is restructured as a GEMM. Write k = (u, s, b) with u the
+// upper prefix (k_0..k_{D-3}), s = k_{D-2}, b = k_{D-1}. For the index sets the
+// solver builds (full, total degree, hyperbolic), the (s, b) sets of the groups
+// u form a chain, so with one shared order of the (s, b) pairs every group is a
+// prefix of length T_u (host.cpp build_mma_layout verifies this). Then
+//
+//   y(x) = sum_u U_u(x) C_u(x),  U_u = prod_{l<D-2} c_{k_l}(x_l),
+//   C_u(x) = sum_{t < T_u} A_t(x) alpha'_{u,t},  A_t = c_{s_t}(x_{D-2}) c_{b_t}(x_{D-1}),
+//
+// and C = A * alpha' is a dense GEMM [paths x terms] x [terms x groups] with a
+// staircase K extent, run as mma.sync.m8n8k4.f64 (8 paths x 8 groups x 4
+// terms). The host sorts groups by T_u, cuts them into 8-group column blocks
+// of 4-term chunks, and forms units (<= kMmaBundle column blocks of equal chunk
+// count x a chunk range of <= kMmaKSplit) balanced over the warps. Each warp
+// runs the DMMAs of its units for all the CTA's paths and folds C into y
+// through U at the end of every unit (C is linear in the chunk range, so a
+// column block can be split across warps with no reduction of C). Each warp
+// streams its own B fragments (32 doubles in lane order) through a private
+// shared-memory ring with cp.async, so the GEMM phase has no CTA barrier; the
+// per-path cosine tables c_k(x_l), k <= kmax_l, live in shared memory.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "qrmc_device.cuh"
+#include "series_block.cuh"
+
+namespace qrmc_dev {
+
+namespace {
+
+constexpr int kThreads = kMmaWarps * 32;
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// u64 draw number idx of a stream (RngStream order: two draws per Philox block,
+// low half first; rng.hpp:60-75), without walking the stream.
+__device__ __forceinline__ uint64_t stream_u64_at(uint64_t seed, uint64_t sid, uint64_t idx) {
+    const uint64_t block = idx >> 1;
+    const uint4 o = philox4x32_10(
+        make_uint4(static_cast<uint32_t>(block), static_cast<uint32_t>(block >> 32), static_cast<uint32_t>(sid),
+                   static_cast<uint32_t>(sid >> 32)),
+        make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)));
+    return (idx & 1) ? ((static_cast<uint64_t>(o.w) << 32) | o.z) : ((static_cast<uint64_t>(o.y) << 32) | o.x);
+}
+__device__ __forceinline__ double u64_to_uniform(uint64_t v) {
+    return DMUL(DADD(static_cast<double>(v >> 12), 0.5), 0x1p-52);
+}
+
+__device__ __forceinline__ int64_t owned_path(const StepArgs& a, int64_t q) {
+    const int64_t cq = q / kChunk;
+    const int64_t r = cq / a.owned_lanes;
+    const int64_t lane = a.lane_lo + cq % a.owned_lanes;
+    return (r * kLanes + lane) * kChunk + q % kChunk;
+}
+
+template <int D>
+struct MmaSmem {
+    double ring[kMmaWarps][kMmaRingFrags * 32];
+    double xj[kMmaPaths][D], xn[kMmaPaths][D];
+    double theta[kMmaPaths][D];
+    double w0[kMmaPaths], dsum[kMmaPaths];
+    double ypart[kMmaWarps][kMmaPaths];
+    int bad[kMmaPaths];
+    int abort;
+    // followed by the cosine tables [table_len][kTabStride] (c_k(x_l) of path p at
+    // (offset_l + k) * kTabStride + p)
+};
+
+template <int D>
+__device__ __forceinline__ double* mma_tables(unsigned char* base) {
+    return reinterpret_cast<double*>(base + ((sizeof(MmaSmem<D>) + 15) & ~size_t{15}));
+}
+
+// A warp's private fragment stream: series s = 0..n_series-1 (alpha_{i+1+s}),
+// each the warp's `frags` fragments (a multiple of kMmaRingFrags; no unit step
+// straddles a ring wrap), copied in batches of kMmaBatch through a ring of
+// kMmaRingBatches slots.
+struct WarpStream {
+    const double* src;  // alpha + (i+1) * row_len + frag_offset * 32
+    int64_t row_len;
+    double* ring;
+    uint32_t per;       // batches per series
+    uint32_t total;     // batches over all series
+    uint32_t issued, landed;
+    uint32_t ready;     // fragments landed: landed * kMmaBatch
+    uint32_t refill_at; // stream position that frees the next slot
+    int lane;
+
+    __device__ __forceinline__ void issue() {
+        const uint32_t s = issued / per, b = issued - s * per;
+        const double* g = src + s * row_len + static_cast<int64_t>(b) * (kMmaBatch * 32);
+        double* d = ring + (issued % kMmaRingBatches) * (kMmaBatch * 32);
+#pragma unroll
+        for (int c = 0; c < kMmaBatch * 32 / 2 / 32; ++c) cp_async16(d + 2 * (c * 32 + lane), g + 2 * (c * 32 + lane));
+        cp_async_commit();
+        ++issued;
+        refill_at += kMmaBatch;
+    }
+    // make fragments [.., upto) visible to the whole warp
+    __device__ __forceinline__ void land(uint32_t upto) {
+        if (upto <= ready) return;
+        do {
+            switch (issued - landed - 1) {
+                case 0: cp_async_wait<0>(); break;
+                case 1: cp_async_wait<1>(); break;
+                case 2: cp_async_wait<2>(); break;
+                default: cp_async_wait<3>(); break;
+            }
+            ++landed;
+            ready += kMmaBatch;
+        } while (upto > ready);
+        __syncwarp();
+    }
+    // fragments below `consumed` are read: refill the freed slots
+    __device__ __forceinline__ void refill(uint32_t consumed) {
+        if (consumed >= refill_at && issued < total) {
+            __syncwarp();
+            do issue(); while (consumed >= refill_at && issued < total);
+        }
+    }
+};
+
+// one unit: NB column blocks x chunks [c0, c1), then y += U * C. Tables are
+// laid out [k][path] with stride kTabStride, the ring as [frag][lane].
+constexpr int kTabStride = kMmaTabStride;
+
+template <int D, int NB>
+__device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int c1, uint32_t& fpos, WarpStream& ws,
+                                         const double* tab, int lane, double (&y)[kMmaRowBlocks]) {
+    constexpr int RB = kMmaRowBlocks;
+    const int row = lane >> 2, col = lane & 3;
+    double acc[RB][NB][2];
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) acc[r][i][0] = acc[r][i][1] = 0.0;
+    const double* trow = tab + row;
+    const double* ring = ws.ring + lane;
+    const uint32_t* term = m.terms + 4 * c0 + col;
+    auto step = [&](uint32_t f) {
+        const uint32_t tp = __ldg(term);
+        term += 4;
+        const double* ps = trow + (tp & 0xFFFFu);
+        const double* pb = trow + (tp >> 16);
+        double a[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) a[r] = DMUL(ps[8 * r], pb[8 * r]);
+        const double* rb = ring + (f % kMmaRingFrags) * 32;
+        double b[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) b[i] = rb[32 * i];
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+#pragma unroll
+            for (int r = 0; r < RB; ++r) dmma(acc[r][i], a[r], b[i]);
+    };
+    constexpr uint32_t W = NB == 3 ? 4 : NB;  // fragment slots per step (host.cpp build_mma_layout)
+    fpos = (fpos + W - 1) / W * W;
+    int c = c0;
+    for (; c + 1 < c1; c += 2) {
+        ws.land(fpos + 2 * W);
+        step(fpos);
+        step(fpos + W);
+        fpos += 2 * W;
+        ws.refill(fpos);
+    }
+    if (c < c1) {
+        ws.land(fpos + W);
+        step(fpos);
+        fpos += W;
+        ws.refill(fpos);
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int g = 8 * (cb0 + i) + 2 * col + h;
+            const double* pu[D - 2];
+#pragma unroll
+            for (int l = 0; l < D - 2; ++l) pu[l] = trow + __ldg(&m.gk[g * (D - 2) + l]);
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                double u = pu[0][8 * r];
+#pragma unroll
+                for (int l = 1; l < D - 2; ++l) u = DMUL(u, pu[l][8 * r]);
+                y[r] = fma(u, acc[r][i][h], y[r]);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) k_responses_mma(const StepArgs a, const MmaArgs m) {
+    static_assert(D >= 3, "the tensor-core K1 needs an upper prefix");
+    static_assert(kMmaPaths * D <= kThreads, "one (path, coordinate) task per thread");
+    extern __shared__ __align__(16) unsigned char dsm[];
+    MmaSmem<D>& sm = *reinterpret_cast<MmaSmem<D>*>(dsm);
+    double* tabs = mma_tables<D>(dsm);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) sm.abort = *a.abort_flag;
+    __syncthreads();
+    if (sm.abort) return;
+
+    const int64_t q0 = static_cast<int64_t>(blockIdx.x) * kMmaPaths;
+    const int4 wi = __ldg(&m.warp_info[warp]);  // {unit_begin, unit_end, frag_offset, frags}
+    WarpStream ws;
+    ws.src = m.alpha + static_cast<int64_t>(a.step + 1) * m.row_len + static_cast<int64_t>(wi.z) * 32;
+    ws.row_len = m.row_len;
+    ws.ring = sm.ring[warp];
+    ws.per = static_cast<uint32_t>(wi.w) / kMmaBatch;
+    ws.total = static_cast<uint32_t>(a.steps - 1 - a.step) * ws.per;
+    ws.issued = 0;
+    ws.landed = 0;
+    ws.ready = 0;
+    ws.refill_at = 0;
+    ws.lane = lane;
+    while (ws.issued < ws.total && ws.issued < kMmaRingBatches) ws.issue();
+    ws.refill_at = 8;  // the fifth batch needs the first one consumed
+
+    // start points X_i ~ nu: draws 0..D-1 of the path's stream (solver.cpp:150-152)
+    const int tp = tid / D, tl = tid % D;
+    const bool task = tid < kMmaPaths * D;
+    const int64_t tq = q0 + tp;
+    const uint64_t tsid = sid_training(a.step, static_cast<uint64_t>(owned_path(a, tq < a.n_owned ? tq : 0)));
+    if (task) {
+        const double x = measure_inv_cdf(a.meas, u64_to_uniform(stream_u64_at(a.seed, tsid, tl)), tl);
+        sm.xj[tp][tl] = x;
+        if (a.cloud && tq < a.n_owned) a.cloud[tl * a.n_owned + tq] = x;
+    }
+    __syncthreads();
+    uint32_t apps = 0, clipped = 0;
+    if (tid < kMmaPaths) {
+        double x[D];
+#pragma unroll
+        for (int l = 0; l < D; ++l) x[l] = sm.xj[tid][l];
+        sm.w0[tid] = damping_weight<D>(x, a.q);
+        sm.dsum[tid] = 0.0;
+        sm.bad[tid] = 0;
+    }
+
+    for (int j = a.step; j < a.steps; ++j) {
+        const bool last = j + 1 == a.steps;
+        // Euler step of coordinate tl (sde.cpp:37-73): draw D + (j-i)*D + tl
+        if (task) {
+            const double nrm = qrmc_normal_quantile(
+                u64_to_uniform(stream_u64_at(a.seed, tsid, static_cast<uint64_t>(D) * (j - a.step + 1) + tl)));
+            const double dw = DMUL(a.sqrt_dt, nrm);
+            const double out = a.prob.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(a.prob.sigma, dw) : dw;
+            const double xo = sm.xj[tp][tl];
+            const double v = a.prob.drift_kind == QRMC_DRIFT_CONST ? DADD(xo, DADD(DMUL(a.prob.drift_c, a.dt), out))
+                                                                   : DADD(xo, out);
+            sm.xn[tp][tl] = v;
+            if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[tp] == 0) sm.bad[tp] = j + 1;
+            if (!last) sm.theta[tp][tl] = DMUL(3.14159265358979323846, measure_cdf(a.meas, v, tl));
+        }
+        __syncthreads();
+        if (!last) {
+            // cosine tables c_k(x_l) = cos(k theta_l): two half-range recurrences per
+            // (path, coordinate), the second restarted from direct cosines
+            for (int t = tid; t < 2 * kMmaPaths * D; t += kThreads) {
+                const int half = t & 1, p = (t >> 1) / D, l = (t >> 1) % D;
+                const double th = sm.theta[p][l];
+                double* tb = tabs + m.offset[l] * kTabStride + p;
+                const int kmax = m.kmax[l];
+                const int k0 = kmax >= 8 ? kmax / 2 : kmax + 1;
+                if (half == 0) {
+                    const double c1 = cos(th), two = DMUL(2.0, c1);
+                    tb[0] = 1.0;
+                    if (kmax >= 1) tb[kTabStride] = c1;
+                    double prev = 1.0, cur = c1;
+                    for (int k = 2; k < k0; ++k) {
+                        const double nx = fma(two, cur, -prev);
+                        prev = cur;
+                        cur = nx;
+                        tb[k * kTabStride] = nx;
+                    }
+                } else if (k0 <= kmax) {
+                    const double two = DMUL(2.0, cos(th));
+                    double prev = cos(static_cast<double>(k0 - 1) * th), cur = cos(static_cast<double>(k0) * th);
+                    tb[k0 * kTabStride] = cur;
+                    for (int k = k0 + 1; k <= kmax; ++k) {
+                        const double nx = fma(two, cur, -prev);
+                        prev = cur;
+                        cur = nx;
+                        tb[k * kTabStride] = nx;
+                    }
+                }
+            }
+            double y[kMmaRowBlocks];
+#pragma unroll
+            for (int r = 0; r < kMmaRowBlocks; ++r) y[r] = 0.0;
+            __syncthreads();  // tables built
+            uint32_t fpos = static_cast<uint32_t>(j - a.step) * static_cast<uint32_t>(wi.w);  // stream position of this series
+            ws.refill(fpos);  // the previous series' padding counts as consumed
+            for (int u = wi.x; u < wi.y; ++u) {
+                const int4 un = __ldg(&m.units[u]);
+                switch (un.y) {
+                    case 1: run_unit<D, 1>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                    case 2: run_unit<D, 2>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                    case 3: run_unit<D, 3>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                    default: run_unit<D, 4>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kMmaRowBlocks; ++r) {
+                y[r] += __shfl_xor_sync(0xffffffffu, y[r], 1);
+                y[r] += __shfl_xor_sync(0xffffffffu, y[r], 2);
+                if ((lane & 3) == 0) sm.ypart[warp][8 * r + (lane >> 2)] = y[r];
+            }
+        }
+        __syncthreads();
+        if (tid < kMmaPaths) {
+            double xn[D], xj[D];
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                xn[l] = sm.xn[tid][l];
+                xj[l] = sm.xj[tid][l];
+            }
+            double y;
+            if (last) {
+                y = terminal<D>(a.prob, xn);  // exact initialisation at the terminal step (solver.cpp:69-72)
+            } else {
+                double ys = 0.0;
+#pragma unroll
+                for (int w = 0; w < kMmaWarps; ++w) ys += sm.ypart[w][tid];
+                y = DMUL(ys, damping_weight<D>(xn, a.q));
+            }
+            const double c = truncate_soft(y, lstar<D>(a.prob, xn));
+            if (q0 + tid < a.n_owned) {
+                ++apps;
+                if (c != y) ++clipped;
+            }
+            sm.dsum[tid] = DADD(sm.dsum[tid], driver<D>(a.prob, DMUL(static_cast<double>(j), a.dt), xj, c));
+#pragma unroll
+            for (int l = 0; l < D; ++l) sm.xj[tid][l] = xn[l];
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    if (tid < kMmaPaths) {
+        const int64_t q = q0 + tid;
+        if (q < a.n_owned) {
+            if (sm.bad[tid]) {
+                // first error kind wins; SimulationError keeps the smallest step
+                atomicCAS(a.err_flags, 0, QRMC_ESIM);
+                atomicMin(a.err_flags + 1, sm.bad[tid]);
+            } else {
+                double xj[D];
+#pragma unroll
+                for (int l = 0; l < D; ++l) xj[l] = sm.xj[tid][l];
+                const double term = terminal<D>(a.prob, xj);
+                const double v = DDIV(DADD(term, DMUL(a.dt, sm.dsum[tid])), sm.w0[tid]);
+                if (!isfinite(v)) atomicCAS(a.err_flags, 0, QRMC_ENUMERIC);
+                a.resp[q] = v;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            apps += __shfl_down_sync(0xffffffffu, apps, o);
+            clipped += __shfl_down_sync(0xffffffffu, clipped, o);
+        }
+        if (tid == 0 && apps) {
+            atomicAdd(a.counters, static_cast<unsigned long long>(apps));
+            if (clipped) atomicAdd(a.counters + 1, static_cast<unsigned long long>(clipped));
+        }
+    }
+}
+
+size_t responses_mma_smem_bytes(int dim, int table_len) {
+    size_t head = 0;
+    switch (dim) {
+        case 3: head = sizeof(MmaSmem<3>); break;
+        case 4: head = sizeof(MmaSmem<4>); break;
+        case 5: head = sizeof(MmaSmem<5>); break;
+        case 6: head = sizeof(MmaSmem<6>); break;
+        case 7: head = sizeof(MmaSmem<7>); break;
+        case 8: head = sizeof(MmaSmem<8>); break;
+        default: return 0;
+    }
+    return ((head + 15) & ~size_t{15}) + static_cast<size_t>(kTabStride) * table_len * sizeof(double);
+}
+
+template <class Fn>
+static cudaError_t with_kernel(int dim, Fn&& fn) {
+    switch (dim) {
+        case 3: return fn(k_responses_mma<3>);
+        case 4: return fn(k_responses_mma<4>);
+        case 5: return fn(k_responses_mma<5>);
+        case 6: return fn(k_responses_mma<6>);
+        case 7: return fn(k_responses_mma<7>);
+        case 8: return fn(k_responses_mma<8>);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t configure_responses_mma(int dim, size_t smem) {
+    return with_kernel(dim, [&](auto kern) {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    });
+}
+
+cudaError_t launch_responses_mma(const StepArgs& a, const MmaArgs& m, cudaStream_t st) {
+    if (a.n_owned == 0) return cudaSuccess;
+    const size_t smem = responses_mma_smem_bytes(a.prob.dim, m.table_len);
+    const unsigned blocks = static_cast<unsigned>((a.n_owned + kMmaPaths - 1) / kMmaPaths);
+    const cudaError_t e = with_kernel(a.prob.dim, [&](auto kern) {
+        kern<<<blocks, kThreads, smem, st>>>(a, m);
+        return cudaGetLastError();
+    });
+    return e;
+}
+
+}  // namespace qrmc_dev

@@ -30,6 +30,10 @@
 
 #include "kernels.cuh"
 
+#ifndef QRMC_HYP_JOINT
+#define QRMC_HYP_JOINT 1
+#endif
+
 namespace qrmc_dev {
 
 constexpr int kTileA = kSeriesTileA;  // coefficients per shared-memory tile
@@ -43,11 +47,11 @@ struct SeriesSmem {
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void load_tile(SeriesSmem& sm, int buf, const SeriesTiles& st, const double* row,
                                           int t) {
@@ -186,51 +190,145 @@ struct SegState {
 // index set whose upper prefix leaves budget B), are evaluated by fully static
 // straight-line code: no segment dispatch, no loop control, static shared-memory
 // offsets, and the c_0 = 1 leaf/sibling products folded away. These small
-// groups are the most frequent ones (C2: 37% of the terms, C4: 59%).
-constexpr int kHypMaxB = 7;  // needs B + 1 <= S2 and B + 1 <= LT
-
+// groups are the most frequent ones (C2: 50% of the terms for B <= 15, C4: 73%).
+// Siblings 0 and 1 share the longest run (B + 1) and are swept together, with
+// leaf values past the register table continued by the Chebyshev recurrence
+// (computed once for both); siblings past the shared table S2 continue theirs.
 __host__ __device__ constexpr int hyp_run(int B, int s) { return B / (s > 1 ? s : 1) + 1; }
 __host__ __device__ constexpr int hyp_pairs_before(int B, int s) {
     int o = 0;
     for (int t = 0; t < s; ++t) o += (hyp_run(B, t) + 1) / 2;
     return o;
 }
+// the device can run profile B with a leaf table of LT entries
+__host__ __device__ constexpr bool hyp_supported(int B, int LT) {
+    return B >= 1 && B <= kHypMaxB && LT >= 2;
+}
 
-template <int B, int S, int P, int LT>
-__device__ __forceinline__ void hyper_sibling(const double2* ra, const double (&leaf)[P][LT], const double* t2,
-                                              int nt, double (&acc)[P]) {
-    constexpr int R = hyp_run(B, S);
-    constexpr int NP = (R + 1) / 2;
-    constexpr int OFF = hyp_pairs_before(B, S);
-    double z[P];
-#pragma unroll
-    for (int j = 0; j < NP; ++j) {
-        const double2 a = ra[OFF + j];
+template <int B, int P, int S2, int LT>
+struct Hyp {
+    const double2* ra;
+    const double (&leaf)[P][LT];
+    const double (&tl)[P];   // 2 c_{D-1}[1]
+    const double (&t2c)[P];  // 2 c_{D-2}[1]
+    const double* t2;        // t2s + tid
+    int nt;
+    double (&acc)[P];
+
+    __device__ __forceinline__ void first_two() {
+        constexpr int R = B + 1;
+        constexpr int NP = (R + 1) / 2;
+        double z0[P], z1[P], cp[P], cc[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            z[p] = j == 0 ? a.x : fma(a.x, leaf[p][2 * j], z[p]);  // leaf[0] = c_0 = 1
-            if (2 * j + 1 < R) z[p] = fma(a.y, leaf[p][2 * j + 1], z[p]);
+            cp[p] = leaf[p][LT - 2];
+            cc[p] = leaf[p][LT - 1];
         }
-    }
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-        if constexpr (S == 0)
-            acc[p] += z[p];  // c_{D-2}[0] = 1
-        else
-            acc[p] = fma(t2[(S * P + p) * nt], z[p], acc[p]);
+        for (int j = 0; j < NP; ++j) {
+            const double2 a0 = ra[j], a1 = ra[NP + j];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int b = 2 * j + h;
+                if (b < R) {
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        double c;
+                        if (b < LT) {
+                            c = leaf[p][b < LT ? b : 0];
+                        } else {
+                            c = fma(tl[p], cc[p], -cp[p]);
+                            cp[p] = cc[p];
+                            cc[p] = c;
+                        }
+                        const double x0 = h ? a0.y : a0.x, x1 = h ? a1.y : a1.x;
+                        z0[p] = b == 0 ? x0 : fma(x0, c, z0[p]);  // c_0 = 1
+                        z1[p] = b == 0 ? x1 : fma(x1, c, z1[p]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[p] = fma(t2[(1 * P + p) * nt], z1[p], acc[p] + z0[p]);
     }
-    if constexpr (S < B) hyper_sibling<B, S + 1, P, LT>(ra, leaf, t2, nt, acc);
-}
+
+    // c2p, c2c enter as (c_{S2-2}, c_{S2-1}) of level D-2 (the group's g2p, g2c)
+    template <int S>
+    __device__ __forceinline__ void sibling(double (&c2p)[P], double (&c2c)[P]) {
+        constexpr int R = hyp_run(B, S);
+        constexpr int NP = (R + 1) / 2;
+        constexpr int OFF = hyp_pairs_before(B, S);
+        double z[P], cp[P], cc[P];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const double2 a = ra[OFF + j];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int b = 2 * j + h;
+                if (b < R) {
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        double c;
+                        if (b < LT) {
+                            c = leaf[p][b < LT ? b : 0];
+                        } else {  // past the leaf table: Chebyshev recurrence
+                            if (b == LT) {
+                                cp[p] = leaf[p][LT - 2];
+                                cc[p] = leaf[p][LT - 1];
+                            }
+                            c = fma(tl[p], cc[p], -cp[p]);
+                            cp[p] = cc[p];
+                            cc[p] = c;
+                        }
+                        const double x = h ? a.y : a.x;
+                        z[p] = b == 0 ? x : fma(x, c, z[p]);  // c_0 = 1
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            if constexpr (S == 0) {
+                acc[p] += z[p];
+            } else {
+                double ts;
+                if constexpr (S < S2) {
+                    ts = t2[(S * P + p) * nt];
+                } else {
+                    ts = fma(t2c[p], c2c[p], -c2p[p]);
+                    c2p[p] = c2c[p];
+                    c2c[p] = ts;
+                }
+                acc[p] = fma(ts, z[p], acc[p]);
+            }
+        }
+        if constexpr (S < B) sibling<S + 1>(c2p, c2c);
+    }
+
+    __device__ __forceinline__ void run(double (&c2p)[P], double (&c2c)[P]) {
+#if QRMC_HYP_JOINT
+        if constexpr (B + 1 > LT) {  // siblings 0 and 1 share one recurrence past the table
+            first_two();
+            if constexpr (B >= 2) sibling<2>(c2p, c2c);
+            return;
+        }
+#endif
+        sibling<0>(c2p, c2c);
+    }
+};
 
 template <int P, int S2, int LT>
 __device__ __forceinline__ void hyper_group(int B, const double2* ra, const double (&leaf)[P][LT],
-                                            const double* t2, int nt, double (&acc)[P]) {
+                                            const double (&tl)[P], const double (&t2c)[P], const double* t2,
+                                            int nt, double (&c2p)[P], double (&c2c)[P], double (&acc)[P]) {
     switch (B) {
-#define QRMC_HYP(b) \
-    case b:         \
-        if constexpr ((b) + 1 <= S2 && (b) + 1 <= LT) hyper_sibling<b, 0, P, LT>(ra, leaf, t2, nt, acc); \
+#define QRMC_HYP(b)                                                      \
+    case b:                                                              \
+        if constexpr (hyp_supported((b), LT) && S2 >= 2)                 \
+            Hyp<(b), P, S2, LT>{ra, leaf, tl, t2c, t2, nt, acc}.run(c2p, c2c); \
         break;
-        QRMC_HYP(1) QRMC_HYP(2) QRMC_HYP(3) QRMC_HYP(4) QRMC_HYP(5) QRMC_HYP(6) QRMC_HYP(7)
+        QRMC_HYP(1) QRMC_HYP(2) QRMC_HYP(3) QRMC_HYP(4) QRMC_HYP(5) QRMC_HYP(6) QRMC_HYP(7) QRMC_HYP(8)
+        QRMC_HYP(9) QRMC_HYP(10) QRMC_HYP(11) QRMC_HYP(12) QRMC_HYP(13) QRMC_HYP(14) QRMC_HYP(15)
 #undef QRMC_HYP
         default: break;
     }
@@ -342,7 +440,7 @@ __device__ __forceinline__ void series_block(SeriesSmem& sm, double* t2s, const 
             if (h & (1u << 29)) {
                 // hyperbolic-profile group: one word {pair offset, B}, static code
                 const uint32_t w = pw[i++];
-                hyper_group<P, S2, LT>(static_cast<int>(w >> 16), pa + (w & 0x3FFu), leaf, t2s + tid, nt, acc2);
+                hyper_group<P, S2, LT>(static_cast<int>(w >> 16), pa + (w & 0x3FFu), leaf, tl, t2c, t2s + tid, nt, g2p, g2c, acc2);
                 continue;
             }
             SegState<P, S2, LT> ss{leaf, tl, t2c, t2s + tid, nt, g2p, g2c, acc2, acc2b};
