@@ -43,14 +43,14 @@ METRIC = "simulated paths x time-steps per second per full backward solve"
 UNIT = "path-steps/s"
 
 
-def traffic_per_launch():
-    """DRAM bytes (read + write) per k_responses launch from the committed ncu
+def traffic_per_launch(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
     --set full capture of this workload (profiles/roofline_traffic.json), or None."""
     f = ROOT / "profiles" / "roofline_traffic.json"
     if not f.exists():
         return None
     try:
-        return json.loads(f.read_text())["k_responses"]["dram_bytes_per_launch"]
+        return json.loads(f.read_text())[kernel]["dram_bytes_per_launch"]
     except (KeyError, ValueError):
         return None
 
@@ -290,6 +290,7 @@ def run_ours(args) -> int:
         t = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
+    names = [L.qrmc_gpu_plan_kernel_name(plan, w).decode() for w in range(3)]
     L.qrmc_gpu_plan_destroy(plan)
 
     cpu = None
@@ -314,12 +315,12 @@ def run_ours(args) -> int:
             "time_to_solution_s": per_solve,
             "fp64_solve_tflops": solve_tflops,
             "fp64_solve_frac": solve_tflops / pk["fp64_tflops"],
-            "kernel_seconds_per_solve": {"k_responses": kernel_s[0] / args.steps,
-                                         "k_project": kernel_s[1] / args.steps,
-                                         "k_finish_step": kernel_s[2] / args.steps},
-            "roofline": {"kernel": "k_responses", "bound": "fp64", "achieved": achieved,
+            "kernel_seconds_per_solve": {names[0]: kernel_s[0] / args.steps,
+                                         names[1]: kernel_s[1] / args.steps,
+                                         names[2]: kernel_s[2] / args.steps},
+            "roofline": {"kernel": names[0], "bound": "fp64", "achieved": achieved,
                          "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"],
-                         "traffic": traffic_per_launch(),
+                         "traffic": traffic_per_launch(names[0]),
                          "peak_source": "measured FP64 (DMMA 37.1 TF/s) on this pool, profiles/r01_fp64_peak.txt"},
             "e2e": {"value": path_steps(paths_total, n) / e2e_t, "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value)},

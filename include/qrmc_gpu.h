@@ -173,6 +173,10 @@ int64_t qrmc_gpu_plan_basis_size(const qrmc_gpu_plan_t* plan);
  * per_step (steps x 3, row i = cloud step i) or NULL. CUDA-event timed inside the graph. */
 qrmc_status qrmc_gpu_plan_kernel_seconds(const qrmc_gpu_plan_t* plan, double* out3, double* per_step,
                                          char* err, size_t err_len);
+/* Name of the kernel the plan runs for kind `which` (0 phase 1, 1 phase 2,
+ * 2 finish): the tensor-core kernels (k_responses_mma, k_project_mma) when the
+ * index set and shared memory allow them, else the series-program kernels. */
+const char* qrmc_gpu_plan_kernel_name(const qrmc_gpu_plan_t* plan, int which);
 /* Multi-GPU path sharding (host-only, no device needed): rank `rank` of `world`
  * owns the reference's lanes [lane_lo, lane_hi) (LaneLayout, parallel.hpp:20-36:
  * chunk c of 1024 paths belongs to lane c % 256) and n_owned paths. */

@@ -20,8 +20,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libqrmc_gpu.so"
-SOURCES = [CSRC / "kernels.cu", CSRC / "responses_mma.cu", CSRC / "host.cpp"]
-HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "series_block.cuh", ROOT / "include" / "qrmc_gpu.h",
+SOURCES = [CSRC / "kernels.cu", CSRC / "responses_mma.cu", CSRC / "project_mma.cu", CSRC / "host.cpp"]
+HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "series_block.cuh", CSRC / "mma_common.cuh", ROOT / "include" / "qrmc_gpu.h",
            ROOT / "include" / "qrmc_normal_quantile.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -517,6 +517,10 @@ struct MmaLayout {
     std::vector<int32_t> pos;       // k -> position in the per-series stream
     int64_t row_len = 0;
     int64_t frags = 0;              // B fragments per series (useful MACs = K of 256 * frags)
+    // K2 on the tensor cores
+    int proj_parts = 0;
+    std::vector<int4> proj_rects;   // [parts][kProjWarps] {gb0, tb0, ngb | ntb << 8, valid tiles}
+    std::vector<int32_t> proj_out;  // [parts][kProjWarps][kProjTiles][32 lanes][2] -> k, or -1
 };
 
 MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
@@ -555,7 +559,7 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
             if (rank[static_cast<size_t>(at(r, d - 2)) * Bn + at(r, d - 1)] >= gr.n) return L;  // not a prefix
     if (static_cast<int64_t>(offset[d - 1] + Bn) * kMmaTabStride > 0xFFFF) return L;
     auto row_of = [](int entry) { return static_cast<uint32_t>(entry * kMmaTabStride); };
-    const int n_terms = static_cast<int>((order.size() + 3) & ~size_t{3});
+    const int n_terms = static_cast<int>((order.size() + 7) & ~size_t{7});  // K1 reads 4-term chunks, K2 8-term blocks
     L.terms.assign(static_cast<size_t>(n_terms), row_of(offset[d - 2]) | row_of(offset[d - 1]) << 16);
     for (size_t t = 0; t < order.size(); ++t)
         L.terms[t] = row_of(offset[d - 2] + order[t] / Bn) | row_of(offset[d - 1] + order[t] % Bn) << 16;
@@ -596,6 +600,12 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     std::stable_sort(ui.begin(), ui.end(), [&](int32_t x, int32_t y) { return units[x].cost > units[y].cost; });
     std::vector<std::vector<int32_t>> per_warp(kMmaWarps);
     std::vector<double> load(kMmaWarps, 0.0);
+    // the first ceil(paths * d / 32) warps also run the next Euler step
+    // (responses_mma.cu) during the GEMM phase
+#ifndef QRMC_MMA_EULER_COST
+#define QRMC_MMA_EULER_COST 400
+#endif
+    for (int w = 0; w < std::min(kMmaWarps, (kMmaPaths * d + 31) / 32); ++w) load[w] = QRMC_MMA_EULER_COST;
     for (int32_t u : ui) {
         const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
         per_warp[w].push_back(u);
@@ -637,6 +647,71 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
             const int64_t f = frag_at[static_cast<size_t>(cb) * cstride + t / 4];
             if (f < 0) fail(QRMC_ELOGIC, "mma layout: term outside the fragment stream");
             L.pos[static_cast<size_t>(r)] = static_cast<int32_t>(f * 32 + ((n << 2) | (t & 3)));
+        }
+    }
+    // K2 (project_mma.cu): output tiles (group block gb, 8-term block tb) of the
+    // staircase G[u][t], t < T_u, cut into full rectangles of ng x nt tiles
+    // (ng in {1, 2, 4, 8}, ng * nt <= kProjTiles), one per warp, kProjWarps per
+    // CTA part. Group blocks are sorted by T_u, so the staircase is a sequence of
+    // strips of equal width (term blocks).
+    {
+        struct Rect { int gb0, ng, tb0, nt, tiles; };
+        std::vector<int> ntb(static_cast<size_t>(n_cb));
+        for (int cb = 0; cb < n_cb; ++cb) ntb[cb] = static_cast<int>((groups[gi[8 * cb]].n + 7) / 8);
+        std::vector<Rect> rects;
+        for (int g = 0; g < n_cb;) {
+            int h = 1;
+            while (g + h < n_cb && ntb[g + h] == ntb[g]) ++h;
+            const int w = ntb[g];
+            // rows in power-of-two bands; each band cut into ng x (kProjTiles / ng)
+            for (int r0 = 0; r0 < h;) {
+                int ng = kProjTiles;
+                while (ng > h - r0) ng /= 2;
+                const int nt_max = kProjTiles / ng;
+                for (int t0 = 0; t0 < w; t0 += nt_max) {
+                    const int nt = std::min(nt_max, w - t0);
+                    rects.push_back(Rect{g + r0, ng, t0, nt, ng * nt});
+                }
+                r0 += ng;
+            }
+            g += h;
+        }
+        std::stable_sort(rects.begin(), rects.end(), [](const Rect& x, const Rect& y) { return x.tiles > y.tiles; });
+        const int parts = static_cast<int>((rects.size() + kProjWarps - 1) / kProjWarps);
+        // LPT over parts, at most kProjWarps rectangles each
+        std::vector<std::vector<int>> part_r(static_cast<size_t>(parts));
+        std::vector<int> part_load(static_cast<size_t>(parts), 0);
+        for (size_t i = 0; i < rects.size(); ++i) {
+            int best = -1;
+            for (int q = 0; q < parts; ++q)
+                if (static_cast<int>(part_r[q].size()) < kProjWarps && (best < 0 || part_load[q] < part_load[best])) best = q;
+            part_r[best].push_back(static_cast<int>(i));
+            part_load[best] += rects[i].tiles;
+        }
+        L.proj_parts = parts;
+        L.proj_rects.assign(static_cast<size_t>(parts) * kProjWarps, make_int4(0, 0, 1, 0));
+        L.proj_out.assign(static_cast<size_t>(parts) * kProjWarps * kProjTiles * 64, -1);
+        for (int q = 0; q < parts; ++q) {
+            for (size_t w = 0; w < part_r[q].size(); ++w) {
+                const Rect& r = rects[part_r[q][w]];
+                const size_t slot = static_cast<size_t>(q) * kProjWarps + w;
+                L.proj_rects[slot] = make_int4(r.gb0, r.tb0, r.ng | r.nt << 8, r.tiles);
+                for (int ig = 0; ig < r.ng; ++ig) {
+                    for (int n = 0; n < 8; ++n) {  // group row of the tile (lane >> 2)
+                        const int c = 8 * (r.gb0 + ig) + n;
+                        if (c >= static_cast<int>(gi.size())) continue;
+                        const Grp& gr = groups[gi[c]];
+                        for (int64_t row = gr.r0; row < gr.r0 + gr.n; ++row) {
+                            const int t = rank[static_cast<size_t>(at(row, d - 2)) * Bn + at(row, d - 1)];
+                            const int it = t / 8 - r.tb0;
+                            if (it < 0 || it >= r.nt) continue;
+                            // C[row = lane >> 2][col = 2 (lane & 3) + h]
+                            const int col = t % 8, lane = n * 4 + col / 2, h = col % 2;
+                            L.proj_out[(slot * kProjTiles + ig * r.nt + it) * 64 + lane * 2 + h] = static_cast<int32_t>(row);
+                        }
+                    }
+                }
+            }
         }
     }
     L.ok = true;
@@ -717,8 +792,11 @@ struct qrmc_gpu_plan {
     DevBuf<int32_t> d_pack_pos, d_item_k, d_item_len, d_item_leaf, d_item_pre;
     int n_items = 0;
     // tensor-core K1 (responses_mma.cu), when the index set allows it
-    bool use_mma = false;
+    bool use_mma = false, use_proj_mma = false;
     MmaArgs mma{};
+    ProjMmaArgs pmma{};
+    DevBuf<int4> d_pm_rects;
+    DevBuf<int32_t> d_pm_out;
     DevBuf<double> d_alpha_mma;
     DevBuf<int4> d_mma_units, d_mma_warps;
     DevBuf<uint32_t> d_mma_terms;
@@ -797,7 +875,13 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
         mark();
         ProjArgs pa = P.proj;
         pa.partials = P.d_partials.p + static_cast<size_t>(P.session->rank) * P.lanes_per_rank * P.K;
-        cuda_check(launch_project(a, pa, st), "k_project");
+        if (P.use_proj_mma) {
+            ProjMmaArgs pm = P.pmma;
+            pm.partials = pa.partials;
+            cuda_check(launch_project_mma(a, pm, st), "k_project_mma");
+        } else {
+            cuda_check(launch_project(a, pa, st), "k_project");
+        }
         if (world > 1) {
             nccl_check(nccl().AllGather(pa.partials, P.d_partials.p, static_cast<size_t>(P.lanes_per_rank) * P.K,
                                         ncclDouble, P.session->comm, st),
@@ -960,6 +1044,32 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                     m.kmax[l] = pa.kmax[l];
                 }
                 cuda_check(configure_responses_mma(d, smem), "k_responses_mma attributes");
+                // K2 on the tensor cores (QRMC_K2=series forces the series K2)
+                const char* k2 = std::getenv("QRMC_K2");
+                const size_t psmem = project_mma_smem_bytes(off);
+                if (!(k2 && std::strcmp(k2, "series") == 0) && psmem <= static_cast<size_t>(optin) && L.proj_parts > 0) {
+                    P->use_proj_mma = true;
+                    P->d_pm_rects.alloc(L.proj_rects.size());
+                    P->d_pm_rects.upload(L.proj_rects.data(), L.proj_rects.size(), st);
+                    P->d_pm_out.alloc(L.proj_out.size());
+                    P->d_pm_out.upload(L.proj_out.data(), L.proj_out.size(), st);
+                    ProjMmaArgs& pm = P->pmma;
+                    pm.rects = P->d_pm_rects.p;
+                    pm.out = P->d_pm_out.p;
+                    pm.terms = P->d_mma_terms.p;
+                    pm.gk = P->d_mma_gk.p;
+                    pm.scale = P->d_pack_scale.p;
+                    pm.parts = L.proj_parts;
+                    pm.table_len = off;
+                    for (int l = 0; l < d; ++l) {
+                        pm.offset[l] = pa.offset[l];
+                        pm.kmax[l] = pa.kmax[l];
+                    }
+                    pm.basis_size = P->K;
+                    cuda_check(configure_project_mma(d, psmem), "k_project_mma attributes");
+                    P->base.cloud_cos = 1;  // K1 stores cos(pi F(x)) for this K2
+                    P->h2d_bytes += L.proj_rects.size() * sizeof(int4) + L.proj_out.size() * sizeof(int32_t);
+                }
                 P->h2d_bytes += (L.units.size() + L.warp_info.size()) * sizeof(int4) +
                                 L.terms.size() * sizeof(uint32_t) + L.gk.size() * sizeof(uint16_t) +
                                 L.pos.size() * sizeof(int32_t);
@@ -1209,6 +1319,16 @@ qrmc_status qrmc_gpu_plan_io_bytes(const qrmc_gpu_plan_t* plan, uint64_t* h2d, u
     *h2d = plan->h2d_bytes;
     *d2h = plan->d2h_bytes;
     return QRMC_OK;
+}
+
+const char* qrmc_gpu_plan_kernel_name(const qrmc_gpu_plan_t* plan, int which) {
+    if (!plan) return nullptr;
+    switch (which) {
+        case 0: return plan->use_mma ? "k_responses_mma" : "k_responses";
+        case 1: return plan->use_proj_mma ? "k_project_mma" : "k_project";
+        case 2: return "k_finish_step";
+        default: return nullptr;
+    }
 }
 
 void* qrmc_gpu_plan_stream(const qrmc_gpu_plan_t* plan) {

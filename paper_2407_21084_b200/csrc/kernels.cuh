@@ -37,6 +37,7 @@ struct StepArgs {
     SeriesTiles tiles;    // the series program
     double* resp;         // [n_owned]
     double* cloud;        // [dim][n_owned] (store mode) or nullptr (recompute)
+    int cloud_cos;        // the cloud holds cos(pi F_l(x_l)) (tensor-core K1/K2 pair) instead of x
     unsigned long long* counters;  // {applications, clipped}
     int* err_flags;       // {kind, min SimulationError step}
     const int* abort_flag;
@@ -47,18 +48,30 @@ struct StepArgs {
 // them on its own units (column blocks x chunk range), streaming its own
 // coefficient fragments through a private shared-memory ring.
 #ifndef QRMC_MMA_WARPS
-#define QRMC_MMA_WARPS 8
+#define QRMC_MMA_WARPS 16
 #endif
 constexpr int kMmaWarps = QRMC_MMA_WARPS;
-constexpr int kMmaRowBlocks = 4;                 // 8-path row blocks per CTA
+#ifndef QRMC_MMA_RB
+#define QRMC_MMA_RB 4
+#endif
+constexpr int kMmaRowBlocks = QRMC_MMA_RB;       // 8-path row blocks per CTA
 constexpr int kMmaPaths = 8 * kMmaRowBlocks;     // paths per CTA
-constexpr int kMmaBundle = 4;                    // max column blocks per unit
-constexpr int kMmaBatch = 8;                     // fragments per copy batch (2 KiB)
-constexpr int kMmaRingBatches = 4;               // per-warp ring depth
+#ifndef QRMC_MMA_BUNDLE
+#define QRMC_MMA_BUNDLE 2
+#endif
+#ifndef QRMC_MMA_BATCH
+#define QRMC_MMA_BATCH 4
+#endif
+#ifndef QRMC_MMA_RING
+#define QRMC_MMA_RING 4
+#endif
+constexpr int kMmaBundle = QRMC_MMA_BUNDLE;      // max column blocks per unit (1..4)
+constexpr int kMmaBatch = QRMC_MMA_BATCH;        // fragments per copy batch (256 B each)
+constexpr int kMmaRingBatches = QRMC_MMA_RING;   // per-warp ring depth
 constexpr int kMmaRingFrags = kMmaBatch * kMmaRingBatches;
 constexpr int kMmaTabStride = kMmaPaths + 4;    // cosine tables [table entry][path], padded
 #ifndef QRMC_MMA_KSPLIT
-#define QRMC_MMA_KSPLIT 16
+#define QRMC_MMA_KSPLIT 32
 #endif
 constexpr int kMmaKSplit = QRMC_MMA_KSPLIT;      // max chunks per unit
 
@@ -72,6 +85,28 @@ struct MmaArgs {
     int table_len;            // doubles per path table (all coordinates)
     int offset[kMaxDim];      // per-coordinate table offsets
     int kmax[kMaxDim];
+};
+
+// K2 on the FP64 tensor cores (project_mma.cu): per owned lane, the staircase
+// G[u][t] = sum_m S_m U_u(X_m) A_t(X_m) as mma.m8n8k4.f64 (8 groups x 8 terms x
+// 4 paths); each warp keeps one rectangle of <= kProjTiles output tiles in
+// registers over all of the lane's paths.
+constexpr int kProjWarps = 16;
+constexpr int kProjTiles = 8;  // output tiles per warp: ng group blocks x nt term blocks, ng in {1,2,4,8}
+constexpr int kProjBatch = 16;  // paths per shared-memory table batch (double-buffered)
+
+struct ProjMmaArgs {
+    const int4* rects;        // [parts][kProjWarps] {gb0, tb0, ng | nt << 8, tiles} (full rectangles)
+    const int32_t* out;       // [parts][kProjWarps][kProjTiles][64] (tile ig * nt + it) -> k or -1
+    const uint32_t* terms;    // MmaArgs::terms (8-term padded)
+    const uint16_t* gk;       // MmaArgs::gk
+    const double* scale;      // sqrt2^{nnz(k)}
+    int parts;
+    int table_len;
+    int offset[kMaxDim];
+    int kmax[kMaxDim];
+    int64_t basis_size;
+    double* partials;         // [owned_lanes][K]
 };
 
 struct ProjArgs {
@@ -110,6 +145,9 @@ cudaError_t launch_responses_mma(const StepArgs& a, const MmaArgs& m, cudaStream
 size_t project_smem_bytes(const ProjArgs& p);
 cudaError_t configure_project(int dim, size_t smem);
 cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st);
+size_t project_mma_smem_bytes(int table_len);
+cudaError_t configure_project_mma(int dim, size_t smem);
+cudaError_t launch_project_mma(const StepArgs& a, const ProjMmaArgs& p, cudaStream_t st);
 cudaError_t launch_finish(const StepArgs& a, const FinishArgs& f, cudaStream_t st);
 
 cudaError_t launch_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* out,

@@ -1,0 +1,241 @@
+// project_mma.cu -- K2 (phase 2 of backward step i) on the FP64 tensor cores.
+//
+// Same contract as k_project in kernels.cu (proj/src/solver.cpp:180-199): per
+// owned lane, partial[lane][k] = sum over the lane's paths m of S_m phi_k(X_m).
+// With k = (u, s, b) as in responses_mma.cu and phi_k = sqrt2^{nnz(k)}
+// U_u A_t (plain cosines),
+//
+//   G[u][t] = sum_m (S_m U_u(X_m)) A_t(X_m),   t < T_u,
+//
+// is a GEMM [groups x paths] x [paths x terms] with a staircase N extent, run
+// as mma.sync.m8n8k4.f64 with M = 8 groups, N = 8 terms, K = 4 paths. Every
+// warp owns one rectangle of <= kProjRG x kProjRT output tiles (host.cpp
+// build_mma_layout) and keeps it in registers while the CTA streams the lane's
+// paths through shared memory in batches of kProjBatch: per batch, the cosine
+// tables c_k(x_l) of every coordinate are built once ([entry][path] layout as in
+// K1), then each warp forms its W = S * U fragments (per group block) and A
+// fragments (per term block) and issues the DMMAs. The lane's sum over paths is
+// thus a fixed-order tensor-core reduction: deterministic and independent of
+// the GPU count (lanes never split across GPUs).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "mma_common.cuh"
+#include "qrmc_device.cuh"
+
+namespace qrmc_dev {
+
+namespace {
+
+constexpr int kThreads = kProjWarps * 32;
+constexpr int kStride = kProjBatch + 4;  // table row stride (paths), padded
+#ifndef QRMC_PROJ_TSPLIT
+#define QRMC_PROJ_TSPLIT 8
+#endif
+constexpr int kTabSplit = QRMC_PROJ_TSPLIT;
+constexpr int kBatchesPerChunk = kChunk / kProjBatch;
+
+struct ProjSmem {
+    double s[2][kProjBatch];  // S_m of the batch (0 past the chunk's end)
+    // followed by two cosine-table buffers [table_len][kStride]
+};
+
+// batch b of the lane: chunk r = b / kBatchesPerChunk, paths [base, base + n)
+struct Batch {
+    int64_t q0, m0;  // owned index and path number of the first path
+    int n;           // paths (<= 0: past the lane's end)
+};
+
+__device__ __forceinline__ Batch lane_batch(const StepArgs& a, int lane_rel, int b) {
+    const int64_t r = b / kBatchesPerChunk;
+    const int base = (b % kBatchesPerChunk) * kProjBatch;
+    const int64_t c = static_cast<int64_t>(a.lane_lo + lane_rel) + r * kLanes;
+    Batch bt;
+    bt.q0 = (r * a.owned_lanes + lane_rel) * kChunk + base;
+    bt.m0 = c * kChunk + base;
+    const int64_t rem = a.paths - bt.m0;
+    bt.n = static_cast<int>(rem < kProjBatch ? (rem < 0 ? 0 : rem) : kProjBatch);
+    return bt;
+}
+
+}  // namespace
+
+// The batch loop of one warp shape: NG group blocks x up to 8 / NG term blocks.
+template <int D, int NG>
+__device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArgs& p, ProjSmem& sm, double* tabs0,
+                                             size_t tab_elems, int lane_rel, int slot, int4 rc) {
+    constexpr int NT = kProjTiles / NG;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int gb0 = rc.x, tb0 = rc.y, nt = rc.z >> 8;
+    const int row = lane >> 2, col = lane & 3;
+    // the lane's fixed operand rows (K1's offsets are rows x kMmaTabStride):
+    // group u = 8 (gb0 + ig) + row, term t = 8 (tb0 + it) + row
+    int gro[NG][D - 2];
+#pragma unroll
+    for (int ig = 0; ig < NG; ++ig)
+#pragma unroll
+        for (int l = 0; l < D - 2; ++l) gro[ig][l] = __ldg(&p.gk[(8 * (gb0 + ig) + row) * (D - 2) + l]) / kMmaTabStride * kStride;
+    int ts_[NT], tb_[NT];
+#pragma unroll
+    for (int it = 0; it < NT; ++it) {
+        const uint32_t v = it < nt ? __ldg(&p.terms[8 * (tb0 + it) + row]) : 0u;
+        ts_[it] = static_cast<int>(v & 0xFFFFu) / kMmaTabStride * kStride;
+        tb_[it] = static_cast<int>(v >> 16) / kMmaTabStride * kStride;
+    }
+    double acc[NG][NT][2];
+#pragma unroll
+    for (int ig = 0; ig < NG; ++ig)
+#pragma unroll
+        for (int it = 0; it < NT; ++it) acc[ig][it][0] = acc[ig][it][1] = 0.0;
+
+    // table task of this thread: path pt, piece q, coordinate l
+    constexpr int TS = kTabSplit * kProjBatch * D <= kThreads ? kTabSplit : kThreads / (kProjBatch * D);
+    constexpr int kTasks = TS * kProjBatch * D;
+    const int pt = tid % kProjBatch, tq = (tid / kProjBatch) % TS, tl = tid / (kProjBatch * TS);
+    const int64_t chunks_total = (a.paths + kChunk - 1) / kChunk;
+    const int64_t my_chunks = (chunks_total - (a.lane_lo + lane_rel) + kLanes - 1) / kLanes;
+    const int n_batches = static_cast<int>(my_chunks) * kBatchesPerChunk;
+    // cos theta_l (and S) of this thread's task in batch b, fetched a batch ahead
+    auto fetch = [&](int b, double& c1, double& sv) {
+        c1 = 1.0;
+        sv = 0.0;
+        if (b >= n_batches || tid >= kTasks) return;
+        {
+            const Batch bt = lane_batch(a, lane_rel, b);
+            if (pt >= bt.n) return;
+            if (a.cloud && a.cloud_cos) {
+                c1 = a.cloud[tl * a.n_owned + bt.q0 + pt];
+            } else {
+                double xl;
+                if (a.cloud) {
+                    xl = a.cloud[tl * a.n_owned + bt.q0 + pt];
+                } else {
+                    // recompute-from-seeds (solver.cpp:187-193): regenerate X_i
+                    xl = measure_inv_cdf(a.meas,
+                                         u64_to_uniform(stream_u64_at(
+                                             a.seed, sid_training(a.step, static_cast<uint64_t>(bt.m0 + pt)), tl)),
+                                         tl);
+                }
+                c1 = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xl, tl)));
+            }
+            if (tq == 0 && tl == 0) sv = a.resp[bt.q0 + pt];
+        }
+    };
+    auto build = [&](int buf, double c1, double sv) {
+        if (tid >= kTasks) return;
+        cos_table_piece_c(c1, p.kmax[tl], tq, TS, tabs0 + buf * tab_elems + p.offset[tl] * kStride + pt, kStride);
+        if (tq == 0 && tl == 0) sm.s[buf][pt] = sv;
+    };
+
+    double cn, sn;
+    fetch(0, cn, sn);
+    build(0, cn, sn);
+    fetch(1, cn, sn);
+    __syncthreads();
+    for (int b = 0; b < n_batches; ++b) {
+        const int buf = b & 1;
+        // tables of batch b+1 (other buffer) while the tensor cores take batch b
+        if (b + 1 < n_batches) {
+            build(buf ^ 1, cn, sn);
+            fetch(b + 2, cn, sn);
+        }
+        const double* tb = tabs0 + buf * tab_elems;
+        // K = 4 paths per DMMA: path 4 ks + col of the batch
+#pragma unroll
+        for (int ks = 0; ks < kProjBatch / 4; ++ks) {
+            const int m = 4 * ks + col;
+            const double* tm = tb + m;
+            const double sv = sm.s[buf][m];
+            double w[NG];
+#pragma unroll
+            for (int ig = 0; ig < NG; ++ig) {
+                double u = DMUL(sv, tm[gro[ig][0]]);
+#pragma unroll
+                for (int l = 1; l < D - 2; ++l) u = DMUL(u, tm[gro[ig][l]]);
+                w[ig] = u;
+            }
+#pragma unroll
+            for (int it = 0; it < NT; ++it) {
+                if (NT == 1 || it < nt) {
+                    const double bv = DMUL(tm[ts_[it]], tm[tb_[it]]);
+#pragma unroll
+                    for (int ig = 0; ig < NG; ++ig) dmma(acc[ig][it], w[ig], bv);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // partial[lane][k] = sqrt2^{nnz(k)} G[u][t]
+    double* out = p.partials + static_cast<int64_t>(lane_rel) * p.basis_size;
+    const int32_t* om = p.out + static_cast<int64_t>(slot) * kProjTiles * 64;
+#pragma unroll
+    for (int ig = 0; ig < NG; ++ig)
+#pragma unroll
+        for (int it = 0; it < NT; ++it)
+            if (it < nt) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int k = __ldg(&om[(ig * nt + it) * 64 + lane * 2 + h]);
+                    if (k >= 0) out[k] = DMUL(acc[ig][it][h], __ldg(&p.scale[k]));
+                }
+            }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, const ProjMmaArgs p) {
+    static_assert(D >= 3, "the tensor-core K2 needs an upper prefix");
+    static_assert(kProjBatch % 4 == 0 && kChunk % kProjBatch == 0, "batches of whole k-steps inside chunks");
+    static_assert(kProjBatch * D <= kThreads, "one table task per thread");
+    extern __shared__ __align__(16) unsigned char dsm[];
+    ProjSmem& sm = *reinterpret_cast<ProjSmem*>(dsm);
+    double* tabs0 = reinterpret_cast<double*>(dsm + ((sizeof(ProjSmem) + 15) & ~size_t{15}));
+    const size_t tab_elems = static_cast<size_t>(p.table_len) * kStride;
+    const int warp = threadIdx.x >> 5;
+    const int part = blockIdx.x, lane_rel = blockIdx.y;
+    const int slot = part * kProjWarps + warp;
+    const int4 rc = __ldg(&p.rects[slot]);
+    // every warp runs the same batch loop (barriers included); the shape only
+    // sets its register tile. Empty slots carry tiles = 0 and write nothing.
+    switch (rc.z & 0xFF) {
+        case 8: project_rect<D, 8>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
+        case 4: project_rect<D, 4>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
+        case 2: project_rect<D, 2>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
+        default: project_rect<D, 1>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
+    }
+}
+
+size_t project_mma_smem_bytes(int table_len) {
+    return ((sizeof(ProjSmem) + 15) & ~size_t{15}) + 2 * static_cast<size_t>(kStride) * table_len * sizeof(double);
+}
+
+template <class Fn>
+static cudaError_t with_project_kernel(int dim, Fn&& fn) {
+    switch (dim) {
+        case 3: return fn(k_project_mma<3>);
+        case 4: return fn(k_project_mma<4>);
+        case 5: return fn(k_project_mma<5>);
+        case 6: return fn(k_project_mma<6>);
+        case 7: return fn(k_project_mma<7>);
+        case 8: return fn(k_project_mma<8>);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t configure_project_mma(int dim, size_t smem) {
+    return with_project_kernel(dim, [&](auto kern) {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    });
+}
+
+cudaError_t launch_project_mma(const StepArgs& a, const ProjMmaArgs& p, cudaStream_t st) {
+    if (a.owned_lanes == 0 || p.parts == 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>(p.parts), static_cast<unsigned>(a.owned_lanes));
+    return with_project_kernel(a.prob.dim, [&](auto kern) {
+        kern<<<grid, kThreads, project_mma_smem_bytes(p.table_len), st>>>(a, p);
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace qrmc_dev

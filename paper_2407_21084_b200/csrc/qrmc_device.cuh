@@ -153,6 +153,28 @@ __device__ __forceinline__ double driver(const ProblemDev& p, double t, const do
     }
 }
 
+// driver() split into its x-dependent part (evaluated ahead, off the critical
+// path) and the combination with y; driver_apply(p, driver_pre<D>(p, t, x), y)
+// performs exactly driver<D>(p, t, x, y)'s operations.
+template <int D>
+__device__ __forceinline__ double driver_pre(const ProblemDev& p, double t, const double* x) {
+    if (p.driver_kind != QRMC_DRIVER_SIN_BENCH) return 0.0;
+    const double e = exp(DDIV(DMUL(DMUL(DMUL(p.dp1, p.dp1), static_cast<double>(D)), DSUB(t, p.horizon)), 2.0));
+    return DMUL(sin(DMUL(p.dp1, sum_of<D>(x))), e);
+}
+__device__ __forceinline__ double driver_apply(const ProblemDev& p, double pre, double y) {
+    switch (p.driver_kind) {
+        case QRMC_DRIVER_ZERO: return 0.0;
+        case QRMC_DRIVER_CONST: return p.dp0;
+        case QRMC_DRIVER_Y: return y;
+        default: {
+            const double z = DSUB(DSUB(DSUB(y, p.dp0), 1.0), pre);
+            const double zz = DMUL(z, z);
+            return zz < 1.0 ? zz : 1.0;
+        }
+    }
+}
+
 // lstar_bound (sde.cpp:27-35)
 template <int D>
 __device__ __forceinline__ double lstar(const ProblemDev& p, const double* x) {

@@ -30,6 +30,7 @@
 
 #include "kernels.cuh"
 #include "qrmc_device.cuh"
+#include "mma_common.cuh"
 #include "series_block.cuh"
 
 namespace qrmc_dev {
@@ -37,40 +38,21 @@ namespace qrmc_dev {
 namespace {
 
 constexpr int kThreads = kMmaWarps * 32;
-
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(c[0]), "+d"(c[1])
-                 : "d"(a), "d"(b));
-}
-
-// u64 draw number idx of a stream (RngStream order: two draws per Philox block,
-// low half first; rng.hpp:60-75), without walking the stream.
-__device__ __forceinline__ uint64_t stream_u64_at(uint64_t seed, uint64_t sid, uint64_t idx) {
-    const uint64_t block = idx >> 1;
-    const uint4 o = philox4x32_10(
-        make_uint4(static_cast<uint32_t>(block), static_cast<uint32_t>(block >> 32), static_cast<uint32_t>(sid),
-                   static_cast<uint32_t>(sid >> 32)),
-        make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)));
-    return (idx & 1) ? ((static_cast<uint64_t>(o.w) << 32) | o.z) : ((static_cast<uint64_t>(o.y) << 32) | o.x);
-}
-__device__ __forceinline__ double u64_to_uniform(uint64_t v) {
-    return DMUL(DADD(static_cast<double>(v >> 12), 0.5), 0x1p-52);
-}
-
-__device__ __forceinline__ int64_t owned_path(const StepArgs& a, int64_t q) {
-    const int64_t cq = q / kChunk;
-    const int64_t r = cq / a.owned_lanes;
-    const int64_t lane = a.lane_lo + cq % a.owned_lanes;
-    return (r * kLanes + lane) * kChunk + q % kChunk;
-}
+#ifndef QRMC_MMA_UNROLL4
+#define QRMC_MMA_UNROLL4 1
+#endif
+#ifndef QRMC_MMA_TSPLIT
+#define QRMC_MMA_TSPLIT 1
+#endif
+constexpr int kTabSplit = QRMC_MMA_TSPLIT;  // recurrence pieces per (path, coordinate) table
 
 template <int D>
 struct MmaSmem {
     double ring[kMmaWarps][kMmaRingFrags * 32];
-    double xj[kMmaPaths][D], xn[kMmaPaths][D];
+    double x[2][kMmaPaths][D];  // X_j and X_{j+1}, alternating
     double theta[kMmaPaths][D];
     double w0[kMmaPaths], dsum[kMmaPaths];
+    double wq[2][kMmaPaths], lq[2][kMmaPaths], dpre[2][kMmaPaths], term[kMmaPaths];  // x-only parts, by evaluation parity
     double ypart[kMmaWarps][kMmaPaths];
     int bad[kMmaPaths];
     int abort;
@@ -167,8 +149,21 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
             for (int r = 0; r < RB; ++r) dmma(acc[r][i], a[r], b[i]);
     };
     constexpr uint32_t W = NB == 3 ? 4 : NB;  // fragment slots per step (host.cpp build_mma_layout)
+    static_assert((QRMC_MMA_UNROLL4 ? 4 : 2) * W + kMmaBatch - 1 <= kMmaRingFrags,
+                  "the ring must hold a whole step group past any batch boundary");
     fpos = (fpos + W - 1) / W * W;
     int c = c0;
+#if QRMC_MMA_UNROLL4
+    for (; c + 3 < c1; c += 4) {
+        ws.land(fpos + 4 * W);
+        step(fpos);
+        step(fpos + W);
+        step(fpos + 2 * W);
+        step(fpos + 3 * W);
+        fpos += 4 * W;
+        ws.refill(fpos);
+    }
+#endif
     for (; c + 1 < c1; c += 2) {
         ws.land(fpos + 2 * W);
         step(fpos);
@@ -204,9 +199,13 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
 }  // namespace
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) k_responses_mma(const StepArgs a, const MmaArgs m) {
+#ifndef QRMC_MMA_MINB
+#define QRMC_MMA_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const StepArgs a, const MmaArgs m) {
     static_assert(D >= 3, "the tensor-core K1 needs an upper prefix");
     static_assert(kMmaPaths * D <= kThreads, "one (path, coordinate) task per thread");
+    static_assert(kMmaPaths <= 32, "warp 0 holds every path's truncation counters");
     extern __shared__ __align__(16) unsigned char dsm[];
     MmaSmem<D>& sm = *reinterpret_cast<MmaSmem<D>*>(dsm);
     double* tabs = mma_tables<D>(dsm);
@@ -229,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_mma(const StepArgs a,
     ws.refill_at = 0;
     ws.lane = lane;
     while (ws.issued < ws.total && ws.issued < kMmaRingBatches) ws.issue();
-    ws.refill_at = 8;  // the fifth batch needs the first one consumed
+    ws.refill_at = kMmaBatch;  // batch kMmaRingBatches reuses the first slot
 
     // start points X_i ~ nu: draws 0..D-1 of the path's stream (solver.cpp:150-152)
     const int tp = tid / D, tl = tid % D;
@@ -238,81 +237,130 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_mma(const StepArgs a,
     const uint64_t tsid = sid_training(a.step, static_cast<uint64_t>(owned_path(a, tq < a.n_owned ? tq : 0)));
     if (task) {
         const double x = measure_inv_cdf(a.meas, u64_to_uniform(stream_u64_at(a.seed, tsid, tl)), tl);
-        sm.xj[tp][tl] = x;
-        if (a.cloud && tq < a.n_owned) a.cloud[tl * a.n_owned + tq] = x;
+        sm.x[0][tp][tl] = x;
+        if (a.cloud && tq < a.n_owned)
+            a.cloud[tl * a.n_owned + tq] = a.cloud_cos ? cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, x, tl))) : x;
     }
     __syncthreads();
     uint32_t apps = 0, clipped = 0;
     if (tid < kMmaPaths) {
         double x[D];
 #pragma unroll
-        for (int l = 0; l < D; ++l) x[l] = sm.xj[tid][l];
+        for (int l = 0; l < D; ++l) x[l] = sm.x[0][tid][l];
         sm.w0[tid] = damping_weight<D>(x, a.q);
         sm.dsum[tid] = 0.0;
         sm.bad[tid] = 0;
     }
+    __syncthreads();
 
-    for (int j = a.step; j < a.steps; ++j) {
-        const bool last = j + 1 == a.steps;
-        // Euler step of coordinate tl (sde.cpp:37-73): draw D + (j-i)*D + tl
+    // Euler step jj of coordinate tl (sde.cpp:37-73): X_{jj+1} from X_jj, draw
+    // D + (jj-i)*D + tl of the path's stream, and theta_l(X_{jj+1}) when alpha_{jj+1}
+    // is evaluated there. Independent of the series values: it runs ahead.
+    auto euler = [&](int jj) {
         if (task) {
+            const int src = (jj - a.step) & 1;
             const double nrm = qrmc_normal_quantile(
-                u64_to_uniform(stream_u64_at(a.seed, tsid, static_cast<uint64_t>(D) * (j - a.step + 1) + tl)));
+                u64_to_uniform(stream_u64_at(a.seed, tsid, static_cast<uint64_t>(D) * (jj - a.step + 1) + tl)));
             const double dw = DMUL(a.sqrt_dt, nrm);
             const double out = a.prob.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(a.prob.sigma, dw) : dw;
-            const double xo = sm.xj[tp][tl];
+            const double xo = sm.x[src][tp][tl];
             const double v = a.prob.drift_kind == QRMC_DRIFT_CONST ? DADD(xo, DADD(DMUL(a.prob.drift_c, a.dt), out))
                                                                    : DADD(xo, out);
-            sm.xn[tp][tl] = v;
-            if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[tp] == 0) sm.bad[tp] = j + 1;
-            if (!last) sm.theta[tp][tl] = DMUL(3.14159265358979323846, measure_cdf(a.meas, v, tl));
+            sm.x[src ^ 1][tp][tl] = v;
+            if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[tp] == 0) sm.bad[tp] = jj + 1;
+            if (jj + 1 < a.steps) sm.theta[tp][tl] = DMUL(3.14159265358979323846, measure_cdf(a.meas, v, tl));
         }
-        __syncthreads();
-        if (!last) {
-            // cosine tables c_k(x_l) = cos(k theta_l): two half-range recurrences per
-            // (path, coordinate), the second restarted from direct cosines
-            for (int t = tid; t < 2 * kMmaPaths * D; t += kThreads) {
-                const int half = t & 1, p = (t >> 1) / D, l = (t >> 1) % D;
-                const double th = sm.theta[p][l];
-                double* tb = tabs + m.offset[l] * kTabStride + p;
-                const int kmax = m.kmax[l];
-                const int k0 = kmax >= 8 ? kmax / 2 : kmax + 1;
-                if (half == 0) {
-                    const double c1 = cos(th), two = DMUL(2.0, c1);
-                    tb[0] = 1.0;
-                    if (kmax >= 1) tb[kTabStride] = c1;
-                    double prev = 1.0, cur = c1;
-                    for (int k = 2; k < k0; ++k) {
-                        const double nx = fma(two, cur, -prev);
-                        prev = cur;
-                        cur = nx;
-                        tb[k * kTabStride] = nx;
-                    }
-                } else if (k0 <= kmax) {
-                    const double two = DMUL(2.0, cos(th));
-                    double prev = cos(static_cast<double>(k0 - 1) * th), cur = cos(static_cast<double>(k0) * th);
-                    tb[k0 * kTabStride] = cur;
-                    for (int k = k0 + 1; k <= kmax; ++k) {
-                        const double nx = fma(two, cur, -prev);
-                        prev = cur;
-                        cur = nx;
-                        tb[k * kTabStride] = nx;
-                    }
+    };
+    // x-only parts of evaluation jj (path p), one kind per task so that the
+    // transcendental functions run on different warps: 0 weight at X_{jj+1}
+    // (terminal value at X_N), 1 truncation bound at X_{jj+1}, 2 the driver's
+    // x-part at X_jj
+    auto path_part = [&](int jj, int p, int kind) {
+        const int c = (jj - a.step) & 1;
+        double xv[D];
+#pragma unroll
+        for (int l = 0; l < D; ++l) xv[l] = sm.x[kind == 2 ? c : c ^ 1][p][l];
+        if (kind == 0) {
+            if (jj + 1 == a.steps)
+                sm.term[p] = terminal<D>(a.prob, xv);
+            else
+                sm.wq[c][p] = damping_weight<D>(xv, a.q);
+        } else if (kind == 1) {
+            sm.lq[c][p] = lstar<D>(a.prob, xv);
+        } else {
+            sm.dpre[c][p] = driver_pre<D>(a.prob, DMUL(static_cast<double>(jj), a.dt), xv);
+        }
+    };
+    // truncation + driver of evaluation jj (solver.cpp:160-172) for path p
+    auto finish_eval = [&](int jj, int p) {
+        const int c = (jj - a.step) & 1;
+        double y;
+        if (jj + 1 == a.steps) {
+            y = sm.term[p];  // exact initialisation at the terminal step (solver.cpp:69-72)
+        } else {
+            double ys = 0.0;
+#pragma unroll
+            for (int w = 0; w < kMmaWarps; ++w) ys += sm.ypart[w][p];
+            y = DMUL(ys, sm.wq[c][p]);
+        }
+        const double cv = truncate_soft(y, sm.lq[c][p]);
+        if (q0 + p < a.n_owned) {
+            ++apps;
+            if (cv != y) ++clipped;
+        }
+        sm.dsum[p] = DADD(sm.dsum[p], driver_apply(a.prob, sm.dpre[c][p], cv));
+    };
+    // one phase: finish evaluation jj_fin, the x-only parts of evaluation
+    // jj_parts, and the cosine tables c_k(x_l) = cos(k theta_l) of evaluation
+    // jj_tab (kTabSplit Chebyshev pieces per (path, coordinate); lanes on
+    // consecutive paths: conflict-free [k][path] stores). Every 32-task group is
+    // one warp's work.
+    auto tables_and_paths = [&](int jj_tab, int jj_fin, int jj_parts) {
+        constexpr int kPathTasks = 4 * kMmaPaths;
+        const int n_tab = jj_tab >= 0 ? kTabSplit * kMmaPaths * D : 0;
+        for (int t = tid; t < kPathTasks + n_tab; t += kThreads) {
+            if (t < kPathTasks) {
+                // finish on warp 0 (it holds the truncation counters), parts on warps 1-3
+                const int p = t % kMmaPaths, kind = t / kMmaPaths;
+                if (kind == 0) {
+                    if (jj_fin >= 0) finish_eval(jj_fin, p);
+                } else if (jj_parts >= 0) {
+                    path_part(jj_parts, p, kind - 1);
                 }
+                continue;
             }
+            const int tt = t - kPathTasks;
+            const int p = tt % kMmaPaths, q = (tt / kMmaPaths) % kTabSplit, l = tt / (kMmaPaths * kTabSplit);
+            cos_table_piece(sm.theta[p][l], m.kmax[l], q, kTabSplit, tabs + m.offset[l] * kTabStride + p, kTabStride);
+        }
+    };
+
+    euler(a.step);
+    __syncthreads();
+    tables_and_paths(a.step + 1 < a.steps ? a.step : -1, -1, a.step);
+    __syncthreads();
+    for (int j = a.step; j < a.steps; ++j) {
+        if (j + 1 < a.steps) {
+            // evaluation of alpha_{j+1} at X_{j+1}; the task warps first run the
+            // next Euler step (the host gives them correspondingly less GEMM work)
+            euler(j + 1);
             double y[kMmaRowBlocks];
 #pragma unroll
             for (int r = 0; r < kMmaRowBlocks; ++r) y[r] = 0.0;
-            __syncthreads();  // tables built
             uint32_t fpos = static_cast<uint32_t>(j - a.step) * static_cast<uint32_t>(wi.w);  // stream position of this series
             ws.refill(fpos);  // the previous series' padding counts as consumed
             for (int u = wi.x; u < wi.y; ++u) {
                 const int4 un = __ldg(&m.units[u]);
-                switch (un.y) {
-                    case 1: run_unit<D, 1>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
-                    case 2: run_unit<D, 2>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
-                    case 3: run_unit<D, 3>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
-                    default: run_unit<D, 4>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                if (un.y == 1) {
+                    run_unit<D, 1>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y);
+                } else if constexpr (kMmaBundle == 2) {
+                    run_unit<D, 2>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y);
+                } else if constexpr (kMmaBundle > 2) {
+                    switch (un.y) {
+                        case 2: run_unit<D, 2>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                        case 3: run_unit<D, 3>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                        default: run_unit<D, kMmaBundle>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y); break;
+                    }
                 }
             }
 #pragma unroll
@@ -321,36 +369,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_mma(const StepArgs a,
                 y[r] += __shfl_xor_sync(0xffffffffu, y[r], 2);
                 if ((lane & 3) == 0) sm.ypart[warp][8 * r + (lane >> 2)] = y[r];
             }
+            __syncthreads();
         }
-        __syncthreads();
-        if (tid < kMmaPaths) {
-            double xn[D], xj[D];
-#pragma unroll
-            for (int l = 0; l < D; ++l) {
-                xn[l] = sm.xn[tid][l];
-                xj[l] = sm.xj[tid][l];
-            }
-            double y;
-            if (last) {
-                y = terminal<D>(a.prob, xn);  // exact initialisation at the terminal step (solver.cpp:69-72)
-            } else {
-                double ys = 0.0;
-#pragma unroll
-                for (int w = 0; w < kMmaWarps; ++w) ys += sm.ypart[w][tid];
-                y = DMUL(ys, damping_weight<D>(xn, a.q));
-            }
-            const double c = truncate_soft(y, lstar<D>(a.prob, xn));
-            if (q0 + tid < a.n_owned) {
-                ++apps;
-                if (c != y) ++clipped;
-            }
-            sm.dsum[tid] = DADD(sm.dsum[tid], driver<D>(a.prob, DMUL(static_cast<double>(j), a.dt), xj, c));
-#pragma unroll
-            for (int l = 0; l < D; ++l) sm.xj[tid][l] = xn[l];
-        }
+        // finish evaluation j; tables and x-only parts of evaluation j+1
+        tables_and_paths(j + 2 < a.steps ? j + 1 : -1, j, j + 1 < a.steps ? j + 1 : -1);
         __syncthreads();
     }
     cp_async_wait<0>();
+    const int cur = (a.steps - a.step) & 1;  // X_N
     if (tid < kMmaPaths) {
         const int64_t q = q0 + tid;
         if (q < a.n_owned) {
@@ -359,20 +385,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_mma(const StepArgs a,
                 atomicCAS(a.err_flags, 0, QRMC_ESIM);
                 atomicMin(a.err_flags + 1, sm.bad[tid]);
             } else {
-                double xj[D];
+                double xN[D];
 #pragma unroll
-                for (int l = 0; l < D; ++l) xj[l] = sm.xj[tid][l];
-                const double term = terminal<D>(a.prob, xj);
+                for (int l = 0; l < D; ++l) xN[l] = sm.x[cur][tid][l];
+                const double term = terminal<D>(a.prob, xN);
                 const double v = DDIV(DADD(term, DMUL(a.dt, sm.dsum[tid])), sm.w0[tid]);
                 if (!isfinite(v)) atomicCAS(a.err_flags, 0, QRMC_ENUMERIC);
                 a.resp[q] = v;
             }
         }
+    }
+    // truncation counters: warp 0 holds them (paths < 32), one atomic per CTA
+    if (warp == 0) {
         for (int o = 16; o > 0; o >>= 1) {
             apps += __shfl_down_sync(0xffffffffu, apps, o);
             clipped += __shfl_down_sync(0xffffffffu, clipped, o);
         }
-        if (tid == 0 && apps) {
+        if (lane == 0 && apps) {
             atomicAdd(a.counters, static_cast<unsigned long long>(apps));
             if (clipped) atomicAdd(a.counters + 1, static_cast<unsigned long long>(clipped));
         }

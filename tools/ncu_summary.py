@@ -19,6 +19,8 @@ KEYS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe inst % of peak"),
+    ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "FP64 tensor (DMMA) pipe active %"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA inst % of peak"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "DFMA thread-instructions"),
     ("dram__bytes_read.sum", "DRAM read"),
