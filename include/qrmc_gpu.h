@@ -173,6 +173,16 @@ int64_t qrmc_gpu_plan_basis_size(const qrmc_gpu_plan_t* plan);
  * per_step (steps x 3, row i = cloud step i) or NULL. CUDA-event timed inside the graph. */
 qrmc_status qrmc_gpu_plan_kernel_seconds(const qrmc_gpu_plan_t* plan, double* out3, double* per_step,
                                          char* err, size_t err_len);
+/* Host-only check of the tensor-core layout (no device needed): builds the
+ * index set and the K1/K2 fragment layouts make_plan would use, replays both
+ * kernels' data flow on the host for one random point and random coefficients,
+ * and returns the relative deviation from the direct sum over Gamma.
+ * info[8] = {layout used (0: series-program kernels), K, K1 units, K1 fragments
+ * per series, fragments the replay read, stream length (fragments, padded),
+ * K2 CTA parts, (s, b) term-table length}. Throws QRMC_ELOGIC on a layout
+ * inconsistency (position clash, missed term, stream overrun). */
+qrmc_status qrmc_gpu_mma_layout_check(int32_t kind, int32_t dim, const int32_t* degrees, int32_t n_degrees,
+                                      uint64_t seed, int64_t* info, double* max_rel_err, char* err, size_t err_len);
 /* Name of the kernel the plan runs for kind `which` (0 phase 1, 1 phase 2,
  * 2 finish): the tensor-core kernels (k_responses_mma, k_project_mma) when the
  * index set and shared memory allow them, else the series-program kernels. */

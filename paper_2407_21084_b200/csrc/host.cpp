@@ -600,16 +600,46 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     std::stable_sort(ui.begin(), ui.end(), [&](int32_t x, int32_t y) { return units[x].cost > units[y].cost; });
     std::vector<std::vector<int32_t>> per_warp(kMmaWarps);
     std::vector<double> load(kMmaWarps, 0.0);
-    // the first ceil(paths * d / 32) warps also run the next Euler step
-    // (responses_mma.cu) during the GEMM phase
+    // the first warps also run the next Euler step and x-only parts during the
+    // GEMM phase
 #ifndef QRMC_MMA_EULER_COST
-#define QRMC_MMA_EULER_COST 400
+#define QRMC_MMA_EULER_COST 800
 #endif
-    for (int w = 0; w < std::min(kMmaWarps, (kMmaPaths * d + 31) / 32); ++w) load[w] = QRMC_MMA_EULER_COST;
-    for (int32_t u : ui) {
-        const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-        per_warp[w].push_back(u);
-        load[w] += units[u].cost;
+    // (responses_mma.cu kAheadThreads: the Euler tasks and the x-only parts)
+    for (int w = 0; w < std::min(kMmaWarps, (std::max(kMmaPaths * d, 3 * kMmaPaths) + 31) / 32); ++w)
+        load[w] = QRMC_MMA_EULER_COST;
+    // Warp w issues on SM sub-partition w % 4, whose DMMA pipe its warps share:
+    // balance the four sub-partitions first (LPT), then the warps inside each.
+#ifndef QRMC_MMA_SMSP_BALANCE
+#define QRMC_MMA_SMSP_BALANCE 1
+#endif
+    constexpr int kSub = QRMC_MMA_SMSP_BALANCE ? 4 : 1;
+    std::vector<std::vector<int32_t>> per_sub(kSub);
+    {
+        std::vector<double> sl(kSub, 0.0);
+        for (int w = 0; w < kMmaWarps; ++w) sl[w % kSub] += load[w];
+        for (int32_t u : ui) {
+            const int b = static_cast<int>(std::min_element(sl.begin(), sl.end()) - sl.begin());
+            per_sub[b].push_back(u);
+            sl[b] += units[u].cost;
+        }
+    }
+    for (int b = 0; b < kSub; ++b) {
+        for (int32_t u : per_sub[b]) {  // still in descending cost order
+            int w = b;
+            for (int v = b; v < kMmaWarps; v += kSub)
+                if (load[v] < load[w]) w = v;
+            per_warp[w].push_back(u);
+            load[w] += units[u].cost;
+        }
+    }
+    if (std::getenv("QRMC_DEBUG_LAYOUT")) {
+        for (int w = 0; w < kMmaWarps; ++w) {
+            std::fprintf(stderr, "warp %2d load %8.0f:", w, load[w]);
+            for (int32_t u : per_warp[w])
+                std::fprintf(stderr, " [cb%d nb%d c%d-%d]", units[u].cb0, units[u].nb, units[u].c0, units[u].c1);
+            std::fprintf(stderr, "\n");
+        }
     }
     std::vector<int64_t> frag_at(static_cast<size_t>(n_cb) * cb_chunks[0], -1);
     const int cstride = cb_chunks[0];
@@ -626,11 +656,11 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
             // a step takes 1, 2 or 4 fragment slots (3 column blocks use 4), aligned,
             // so no step straddles the ring wrap
             const int stride = un.nb == 3 ? 4 : un.nb;
+            L.frags += static_cast<int64_t>(un.nb) * (un.c1 - un.c0);
             f = (f + stride - 1) / stride * stride;
             for (int c = un.c0; c < un.c1; ++c, f += stride)
                 for (int i = 0; i < un.nb; ++i) frag_at[static_cast<size_t>(un.cb0 + i) * cstride + c] = woff + f + i;
         }
-        L.frags += f;
         const int64_t fpad = (f + kMmaRingFrags - 1) / kMmaRingFrags * kMmaRingFrags;
         L.warp_info.push_back(make_int4(ub, static_cast<int>(L.units.size()), static_cast<int>(woff), static_cast<int>(fpad)));
         woff += fpad;
@@ -1211,6 +1241,132 @@ qrmc_status qrmc_gpu_gamma_indices(int32_t kind, int32_t dim, const int32_t* deg
         const Gamma g = build_gamma(kind, dim, degrees, n_degrees);
         if (!out || out_len < g.rows.size()) fail(QRMC_EINVAL, "output buffer too small");
         std::memcpy(out, g.rows.data(), g.rows.size() * sizeof(int32_t));
+    });
+}
+
+qrmc_status qrmc_gpu_mma_layout_check(int32_t kind, int32_t dim, const int32_t* degrees, int32_t n_degrees,
+                                      uint64_t seed, int64_t* info, double* max_rel_err, char* err, size_t err_len) {
+    return guarded(err, err_len, [&] {
+        if (!info || !max_rel_err) fail(QRMC_EINVAL, "null output");
+        const Gamma g = build_gamma(kind, dim, degrees, n_degrees);
+        const int d = g.dim;
+        const int64_t K = g.size();
+        int offset[kMaxDim] = {}, off = 0;
+        for (int l = 0; l < d; ++l) {  // make_plan's table layout
+            offset[l] = off;
+            off += (g.kmax[l] + 2) & ~1;
+        }
+        const MmaLayout L = build_mma_layout(g, offset);
+        for (int i = 0; i < 8; ++i) info[i] = 0;
+        *max_rel_err = 0.0;
+        info[0] = L.ok ? 1 : 0;
+        if (!L.ok) return;
+        // random point (cosine tables c_k = cos(k theta_l)) and coefficients
+        uint64_t st = seed * 0x9E3779B97F4A7C15ull + 1;
+        auto rnd = [&] {
+            st ^= st << 13;
+            st ^= st >> 7;
+            st ^= st << 17;
+            return static_cast<double>(st >> 11) * 0x1p-53;
+        };
+        std::vector<double> tab(static_cast<size_t>(off), 0.0);  // entry -> value (one path)
+        for (int l = 0; l < d; ++l) {
+            const double th = 3.141592653589793 * rnd();
+            for (int k = 0; k <= g.kmax[l]; ++k) tab[static_cast<size_t>(offset[l] + k)] = std::cos(k * th);
+        }
+        std::vector<double> alpha(static_cast<size_t>(K));
+        for (auto& a : alpha) a = 2.0 * rnd() - 1.0;
+        auto term = [&](int64_t r) {
+            double v = 1.0;
+            for (int l = 0; l < d; ++l) v *= tab[static_cast<size_t>(offset[l] + g.rows[static_cast<size_t>(r * d + l)])];
+            return v;
+        };
+        double direct = 0.0, scale = 0.0;
+        for (int64_t r = 0; r < K; ++r) {
+            direct += alpha[static_cast<size_t>(r)] * term(r);
+            scale += std::fabs(alpha[static_cast<size_t>(r)] * term(r));
+        }
+        // K1: scatter alpha into one series' fragment stream, then replay the
+        // kernel's traversal (units per warp, step alignment, B lane order,
+        // A from the term table rows, epilogue through the group rows)
+        std::vector<double> stream(static_cast<size_t>(L.row_len), 0.0);
+        std::vector<uint8_t> hit(static_cast<size_t>(L.row_len), 0);
+        for (int64_t r = 0; r < K; ++r) {
+            const int32_t p = L.pos[static_cast<size_t>(r)];
+            if (p < 0 || p >= L.row_len || hit[static_cast<size_t>(p)]) fail(QRMC_ELOGIC, "mma layout: position clash");
+            hit[static_cast<size_t>(p)] = 1;
+            stream[static_cast<size_t>(p)] = alpha[static_cast<size_t>(r)];
+        }
+        auto row_val = [&](uint32_t row_x_stride) { return tab[row_x_stride / kMmaTabStride]; };
+        const int nu = d - 2;
+        double y = 0.0;
+        int64_t frags_read = 0;
+        for (int w = 0; w < kMmaWarps; ++w) {
+            const int4 wi = L.warp_info[static_cast<size_t>(w)];
+            int64_t fpos = 0;
+            for (int u = wi.x; u < wi.y; ++u) {
+                const int4 un = L.units[static_cast<size_t>(u)];
+                const int nb = un.y, W = nb == 3 ? 4 : nb;
+                fpos = (fpos + W - 1) / W * W;
+                std::vector<double> C(static_cast<size_t>(nb) * 8, 0.0);
+                for (int c = un.z; c < un.w; ++c, fpos += W) {
+                    for (int i = 0; i < nb; ++i) {
+                        const double* B = &stream[static_cast<size_t>((wi.z + fpos + i) * 32)];
+                        ++frags_read;
+                        for (int lane = 0; lane < 32; ++lane) {
+                            const int rr = lane & 3, col = lane >> 2;  // B[term rr][group col]
+                            const uint32_t tp = L.terms[static_cast<size_t>(4 * c + rr)];
+                            const double A = row_val(tp & 0xFFFFu) * row_val(tp >> 16);
+                            C[static_cast<size_t>(i * 8 + col)] += A * B[lane];
+                        }
+                    }
+                }
+                for (int i = 0; i < nb; ++i)
+                    for (int n = 0; n < 8; ++n) {
+                        const int grp = 8 * (un.x + i) + n;
+                        double U = 1.0;
+                        for (int l = 0; l < nu; ++l) U *= row_val(L.gk[static_cast<size_t>(grp * nu + l)]);
+                        y += U * C[static_cast<size_t>(i * 8 + n)];
+                    }
+            }
+            if (fpos > wi.w) fail(QRMC_ELOGIC, "mma layout: warp stream overrun");
+        }
+        // K2: one path with S = 1 through every rectangle's output map
+        std::vector<double> part(static_cast<size_t>(K), 0.0);
+        std::vector<uint8_t> khit(static_cast<size_t>(K), 0);
+        for (size_t slot = 0; slot < L.proj_rects.size(); ++slot) {
+            const int4 rc = L.proj_rects[slot];
+            const int ng = rc.z & 0xFF, nt = rc.z >> 8;
+            if (rc.w == 0) continue;
+            for (int ig = 0; ig < ng; ++ig)
+                for (int it = 0; it < nt; ++it)
+                    for (int lane = 0; lane < 32; ++lane)
+                        for (int h = 0; h < 2; ++h) {
+                            const int32_t k = L.proj_out[(slot * kProjTiles + ig * nt + it) * 64 + lane * 2 + h];
+                            if (k < 0) continue;
+                            if (khit[static_cast<size_t>(k)]) fail(QRMC_ELOGIC, "mma layout: K2 output clash");
+                            khit[static_cast<size_t>(k)] = 1;
+                            const int grp = 8 * (rc.x + ig) + (lane >> 2);
+                            const int t = 8 * (rc.y + it) + 2 * (lane & 3) + h;
+                            double U = 1.0;
+                            for (int l = 0; l < nu; ++l) U *= row_val(L.gk[static_cast<size_t>(grp * nu + l)]);
+                            const uint32_t tp = L.terms[static_cast<size_t>(t)];
+                            part[static_cast<size_t>(k)] = U * row_val(tp & 0xFFFFu) * row_val(tp >> 16);
+                        }
+        }
+        double e2 = 0.0;
+        for (int64_t r = 0; r < K; ++r) {
+            if (!khit[static_cast<size_t>(r)]) fail(QRMC_ELOGIC, "mma layout: K2 misses a term");
+            e2 = std::max(e2, std::fabs(part[static_cast<size_t>(r)] - term(r)));
+        }
+        *max_rel_err = std::max(std::fabs(y - direct) / std::max(scale, 1e-300), e2);
+        info[1] = K;
+        info[2] = static_cast<int64_t>(L.units.size());
+        info[3] = L.frags;
+        info[4] = frags_read;
+        info[5] = L.row_len / 32;
+        info[6] = L.proj_parts;
+        info[7] = static_cast<int64_t>(L.terms.size());
     });
 }
 

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "kernels.cuh"
 #include "qrmc_device.cuh"
@@ -38,6 +39,23 @@ namespace qrmc_dev {
 namespace {
 
 constexpr int kThreads = kMmaWarps * 32;
+
+// clock read that stays in place relative to barriers (phase timing experiments)
+__device__ __forceinline__ long long clk_fenced() {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    return t;
+}
+// CTA barrier whose release is observed: the clock read depends on its result
+__device__ __forceinline__ long long sync_clk() {
+    const int n = __syncthreads_count(1);
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : "r"(n) : "memory");
+    return t;
+}
+#ifndef QRMC_MMA_AHEAD
+#define QRMC_MMA_AHEAD 2
+#endif
 #ifndef QRMC_MMA_UNROLL4
 #define QRMC_MMA_UNROLL4 1
 #endif
@@ -206,6 +224,9 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
     static_assert(D >= 3, "the tensor-core K1 needs an upper prefix");
     static_assert(kMmaPaths * D <= kThreads, "one (path, coordinate) task per thread");
     static_assert(kMmaPaths <= 32, "warp 0 holds every path's truncation counters");
+    // threads that run ahead during the GEMM phase (Euler tasks, x-only parts)
+    constexpr int kAheadThreads = ((kMmaPaths * D > 3 * kMmaPaths ? kMmaPaths * D : 3 * kMmaPaths) + 31) / 32 * 32;
+    static_assert(kAheadThreads <= kThreads, "ahead group fits the CTA");
     extern __shared__ __align__(16) unsigned char dsm[];
     MmaSmem<D>& sm = *reinterpret_cast<MmaSmem<D>*>(dsm);
     double* tabs = mma_tables<D>(dsm);
@@ -317,7 +338,11 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
     // one warp's work.
     auto tables_and_paths = [&](int jj_tab, int jj_fin, int jj_parts) {
         constexpr int kPathTasks = 4 * kMmaPaths;
+#ifndef QRMC_MMA_SKIP_TABLES  // timing experiments only
         const int n_tab = jj_tab >= 0 ? kTabSplit * kMmaPaths * D : 0;
+#else
+        const int n_tab = 0;
+#endif
         for (int t = tid; t < kPathTasks + n_tab; t += kThreads) {
             if (t < kPathTasks) {
                 // finish on warp 0 (it holds the truncation counters), parts on warps 1-3
@@ -339,17 +364,37 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
     __syncthreads();
     tables_and_paths(a.step + 1 < a.steps ? a.step : -1, -1, a.step);
     __syncthreads();
+#ifdef QRMC_MMA_PHASE_CLOCKS
+    long long acc_own = 0, acc_gemm = 0, acc_tab = 0;
+    const long long c_k0 = clk_fenced();
+#endif
     for (int j = a.step; j < a.steps; ++j) {
         if (j + 1 < a.steps) {
-            // evaluation of alpha_{j+1} at X_{j+1}; the task warps first run the
-            // next Euler step (the host gives them correspondingly less GEMM work)
-            euler(j + 1);
+            // evaluation of alpha_{j+1} at X_{j+1}. The first kAheadThreads threads
+            // first run the next Euler step and the x-only parts of the next
+            // evaluation (the host gives their warps correspondingly less GEMM work)
+#ifdef QRMC_MMA_PHASE_CLOCKS
+            const long long c_g0 = clk_fenced();
+#endif
+#if QRMC_MMA_AHEAD >= 1
+            if (tid < kAheadThreads) {
+                euler(j + 1);
+#if QRMC_MMA_AHEAD >= 2
+                asm volatile("bar.sync 1, %0;" ::"n"(kAheadThreads) : "memory");
+                if (tid < 3 * kMmaPaths) path_part(j + 1, tid % kMmaPaths, tid / kMmaPaths);
+#endif
+            }
+#endif
             double y[kMmaRowBlocks];
 #pragma unroll
             for (int r = 0; r < kMmaRowBlocks; ++r) y[r] = 0.0;
             uint32_t fpos = static_cast<uint32_t>(j - a.step) * static_cast<uint32_t>(wi.w);  // stream position of this series
             ws.refill(fpos);  // the previous series' padding counts as consumed
+#ifndef QRMC_MMA_SKIP_GEMM  // timing experiments only: phases without the GEMM
             for (int u = wi.x; u < wi.y; ++u) {
+#else
+            for (int u = wi.x; u < wi.x; ++u) {
+#endif
                 const int4 un = __ldg(&m.units[u]);
                 if (un.y == 1) {
                     run_unit<D, 1>(m, un.x, un.z, un.w, fpos, ws, tabs, lane, y);
@@ -369,12 +414,39 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
                 y[r] += __shfl_xor_sync(0xffffffffu, y[r], 2);
                 if ((lane & 3) == 0) sm.ypart[warp][8 * r + (lane >> 2)] = y[r];
             }
+#ifdef QRMC_MMA_PHASE_CLOCKS
+            const long long c_w = clk_fenced();
+            const long long c_g1 = sync_clk();
+#else
             __syncthreads();
+#endif
+#ifdef QRMC_MMA_PHASE_CLOCKS
+            acc_own += c_w - c_g0;
+            acc_gemm += c_g1 - c_g0;
+            if (blockIdx.x == 100 && a.step == 5 && lane == 0 && j == 10)
+                printf("RAW warp=%d g0=%lld w=%lld g1=%lld\n", warp, c_g0, c_w, c_g1);
+#endif
         }
+#ifdef QRMC_MMA_PHASE_CLOCKS
+        const long long c_t0 = clk_fenced();
+#endif
         // finish evaluation j; tables and x-only parts of evaluation j+1
-        tables_and_paths(j + 2 < a.steps ? j + 1 : -1, j, j + 1 < a.steps ? j + 1 : -1);
+#if QRMC_MMA_AHEAD == 0
+        if (j + 1 < a.steps) euler(j + 1);
         __syncthreads();
+#endif
+        tables_and_paths(j + 2 < a.steps ? j + 1 : -1, j, QRMC_MMA_AHEAD >= 2 ? -1 : (j + 1 < a.steps ? j + 1 : -1));
+#ifdef QRMC_MMA_PHASE_CLOCKS
+        acc_tab += sync_clk() - c_t0;
+#else
+        __syncthreads();
+#endif
     }
+#ifdef QRMC_MMA_PHASE_CLOCKS
+    if (blockIdx.x == 100 && a.step == 5 && lane == 0)
+        printf("PHASE warp=%d own=%lld gemm=%lld tables=%lld total=%lld\n", warp, acc_own, acc_gemm, acc_tab,
+               clk_fenced() - c_k0);
+#endif
     cp_async_wait<0>();
     const int cur = (a.steps - a.step) & 1;  // X_N
     if (tid < kMmaPaths) {

@@ -6,10 +6,10 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "u4": (),
-    "u2": ("QRMC_MMA_UNROLL4=0",),
-    "u4k32": ("QRMC_MMA_KSPLIT=32",),
-    "u4k8": ("QRMC_MMA_KSPLIT=8",),
+    "e0": ("QRMC_MMA_EULER_COST=0",),
+    "e200": ("QRMC_MMA_EULER_COST=200",),
+    "e800": (),
+    "ah1e400": ("QRMC_MMA_AHEAD=1", "QRMC_MMA_EULER_COST=400"),
 }
 def one(kv):
     name, defs = kv

@@ -135,3 +135,61 @@ def test_lane_sharding_partitions_paths(paths, world):
     assert total == paths
     if paths <= 262145:
         assert sorted(seen) == list(range(paths))
+
+
+# ---------------------------------------------------------------- tensor-core layout
+# host.cpp build_mma_layout: the fragment streams of the FP64 tensor-core kernels.
+# qrmc_gpu_mma_layout_check replays both kernels' data flow on the host (units,
+# step alignment, mma lane order, term/group table rows, K2 rectangles and output
+# map) for a random point and checks it against the direct sum over Gamma.
+MMA_CASES = [
+    (_abi.GAMMA_HYPERBOLIC, 4, [100]),   # the bench workload (K = 12,752)
+    (_abi.GAMMA_HYPERBOLIC, 4, [16]),
+    (_abi.GAMMA_HYPERBOLIC, 3, [8]),
+    (_abi.GAMMA_HYPERBOLIC, 3, [40]),
+    (_abi.GAMMA_HYPERBOLIC, 5, [20]),
+    (_abi.GAMMA_HYPERBOLIC, 6, [8]),
+    (_abi.GAMMA_HYPERBOLIC, 8, [6]),
+    (_abi.GAMMA_TOTAL, 3, [9]),
+    (_abi.GAMMA_TOTAL, 4, [6]),
+    (_abi.GAMMA_TOTAL, 6, [4]),
+    (_abi.GAMMA_FULL, 3, [3]),
+    (_abi.GAMMA_FULL, 4, [3]),
+    (_abi.GAMMA_FULL, 3, [5, 2, 7]),
+    (_abi.GAMMA_FULL, 5, [1]),
+]
+
+
+def _layout_check(kind, dim, degrees, seed=7):
+    L = _abi.lib()
+    deg = (C.c_int32 * len(degrees))(*degrees)
+    info = (C.c_int64 * 8)()
+    rel = C.c_double()
+    err = C.create_string_buffer(512)
+    st = L.qrmc_gpu_mma_layout_check(kind, dim, deg, len(degrees), seed, info, C.byref(rel), err, 512)
+    assert st == 0, err.value.decode()
+    return list(info), rel.value
+
+
+@pytest.mark.parametrize("kind,dim,degrees", MMA_CASES, ids=lambda v: str(v))
+def test_mma_layout_replays_the_series(kind, dim, degrees):
+    info, rel = _layout_check(kind, dim, degrees)
+    K = _abi.lib().qrmc_gpu_gamma_size(kind, dim, (C.c_int32 * len(degrees))(*degrees), len(degrees))
+    assert info[0] == 1, "chain index sets with d >= 3 take the tensor-core kernels"
+    assert info[1] == K
+    assert info[4] == info[3], "the replay reads every fragment of the stream exactly once"
+    assert info[3] * 32 >= K and info[5] >= info[3]
+    assert rel < 1e-13, rel
+
+
+def test_mma_layout_bench_useful_fraction():
+    # 12,752 useful MACs of 32 per fragment: 83% at the bench configuration
+    info, _ = _layout_check(_abi.GAMMA_HYPERBOLIC, 4, [100])
+    assert 0.80 < 12752 / (32 * info[3]) <= 1.0
+
+
+@pytest.mark.parametrize("kind,dim,degrees", [(_abi.GAMMA_HYPERBOLIC, 2, [10]), (_abi.GAMMA_FULL, 1, [20]),
+                                               (_abi.GAMMA_TOTAL, 2, [7])])
+def test_mma_layout_not_used_below_three_coordinates(kind, dim, degrees):
+    info, rel = _layout_check(kind, dim, degrees)
+    assert info[0] == 0 and rel == 0.0

@@ -228,3 +228,57 @@ def test_statistical_table1_and_table2(L):
     assert sum(q21_av[r] < q0_av[r] for r in range(20)) >= 18
     lo, hi = api.confidence_interval(origin, 0.99)
     assert lo <= 1.6 <= hi and hi - lo <= 0.15
+
+
+# ---------------------------------------------------------------- kernel families
+# d >= 3 plans run the FP64 tensor-core kernels (responses_mma.cu, project_mma.cu);
+# QRMC_K1=series / QRMC_K2=series force the series-program kernels. Both families
+# must reproduce the reference's goldens.
+def _kernel_names(prob, cfg):
+    L = _abi.lib()
+    plan = C.c_void_p()
+    err = C.create_string_buffer(512)
+    assert L.qrmc_gpu_plan_create(None, C.byref(prob), cfg.ref(), C.byref(plan), err, 512) == 0, err.value
+    try:
+        return [L.qrmc_gpu_plan_kernel_name(plan, w).decode() for w in range(3)]
+    finally:
+        L.qrmc_gpu_plan_destroy(plan)
+
+
+@pytest.mark.parametrize("entry", GOLDEN["solves"],
+                         ids=lambda e: e["case"]["name"])
+def test_series_program_kernels_match_reference(L, entry, monkeypatch):
+    case = entry["case"]
+    prob, cfg = build_case(case)
+    monkeypatch.setenv("QRMC_K1", "series")
+    monkeypatch.setenv("QRMC_K2", "series")
+    assert _kernel_names(prob, cfg)[:2] == ["k_responses", "k_project"]
+    coeffs, stats, _ = api.backward_solve(prob, cfg)
+    ref = unhex(entry["coeffs"]).reshape(coeffs.shape)
+    assert alpha_close(coeffs, ref) <= ALPHA_TOL
+    assert stats.applications == entry["applications"]
+    assert stats.clipped == entry["clipped"]
+
+
+@pytest.mark.parametrize("dim,kind,deg", [(3, 2, [8]), (4, 2, [100]), (6, 2, [8]), (4, 1, [6]), (5, 0, [2])])
+def test_tensor_core_kernels_selected(L, dim, kind, deg):
+    prob = _abi.sin_bench_problem(dim)
+    cfg = _abi.ConfigHolder(steps=3, paths=2048, damping=5.1, seed=1, gamma_kind=kind, degrees=deg)
+    assert _kernel_names(prob, cfg) == ["k_responses_mma", "k_project_mma", "k_finish_step"]
+
+
+def test_tensor_core_and_series_kernels_agree(L):
+    # same solve through both kernel families: agreement to rounding
+    prob = _abi.sin_bench_problem(4)
+    cfg = _abi.ConfigHolder(steps=6, paths=30000, damping=5.1, seed=11, gamma_kind=2, degrees=[24])
+    a, sa, _ = api.backward_solve(prob, cfg)
+    import os
+    os.environ["QRMC_K1"] = "series"
+    os.environ["QRMC_K2"] = "series"
+    try:
+        b, sb, _ = api.backward_solve(prob, cfg)
+    finally:
+        del os.environ["QRMC_K1"]
+        del os.environ["QRMC_K2"]
+    assert alpha_close(a, b) <= ALPHA_TOL
+    assert (sa.applications, sa.clipped) == (sb.applications, sb.clipped)
