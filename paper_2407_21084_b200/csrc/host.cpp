@@ -582,16 +582,33 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     // processing time first) with an issue-slot cost model
     struct Unit { int cb0, nb, c0, c1; double cost; };
     std::vector<Unit> units;
-    for (int cb = 0; cb < n_cb;) {
-        int e = cb;
-        while (e < n_cb && e - cb < kMmaBundle && cb_chunks[e] == cb_chunks[cb]) ++e;
-        const int E = cb_chunks[cb], nb = e - cb;
-        const int np = (E + kMmaKSplit - 1) / kMmaKSplit;
+    auto add_units = [&](int cb, int nb, int lo, int hi) {  // chunk range [lo, hi) of cbs cb..cb+nb-1
+        if (hi <= lo) return;
+        const int np = (hi - lo + kMmaKSplit - 1) / kMmaKSplit;
         for (int q = 0; q < np; ++q) {
-            const int c0 = static_cast<int>(static_cast<int64_t>(E) * q / np);
-            const int c1 = static_cast<int>(static_cast<int64_t>(E) * (q + 1) / np);
+            const int c0 = lo + static_cast<int>(static_cast<int64_t>(hi - lo) * q / np);
+            const int c1 = lo + static_cast<int>(static_cast<int64_t>(hi - lo) * (q + 1) / np);
             const double len = c1 - c0;
             units.push_back({cb, nb, c0, c1, len * (16.0 + nb * 10.0) + nb * 48.0});
+        }
+    };
+#ifndef QRMC_MMA_STAIR
+#define QRMC_MMA_STAIR 1
+#endif
+    for (int cb = 0; cb < n_cb;) {
+        int e = cb;
+        if (QRMC_MMA_STAIR) {
+            // staircase bundles: kMmaBundle consecutive column blocks share the chunks
+            // all of them have; each block's remainder runs in narrower units
+            e = std::min(n_cb, cb + kMmaBundle);
+            int lo = 0;
+            for (int k = e; k > cb; --k) {  // blocks cb..k-1 share [lo, E_{k-1})
+                add_units(cb, k - cb, lo, cb_chunks[k - 1]);
+                lo = std::max(lo, cb_chunks[k - 1]);
+            }
+        } else {
+            while (e < n_cb && e - cb < kMmaBundle && cb_chunks[e] == cb_chunks[cb]) ++e;
+            add_units(cb, e - cb, 0, cb_chunks[cb]);
         }
         cb = e;
     }

@@ -48,7 +48,7 @@ struct StepArgs {
 // them on its own units (column blocks x chunk range), streaming its own
 // coefficient fragments through a private shared-memory ring.
 #ifndef QRMC_MMA_WARPS
-#define QRMC_MMA_WARPS 16
+#define QRMC_MMA_WARPS 20
 #endif
 constexpr int kMmaWarps = QRMC_MMA_WARPS;
 #ifndef QRMC_MMA_RB

@@ -56,6 +56,9 @@ __device__ __forceinline__ long long sync_clk() {
 #ifndef QRMC_MMA_AHEAD
 #define QRMC_MMA_AHEAD 2
 #endif
+#ifndef QRMC_MMA_PIPE
+#define QRMC_MMA_PIPE 0
+#endif
 #ifndef QRMC_MMA_UNROLL4
 #define QRMC_MMA_UNROLL4 1
 #endif
@@ -170,6 +173,62 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
     static_assert((QRMC_MMA_UNROLL4 ? 4 : 2) * W + kMmaBatch - 1 <= kMmaRingFrags,
                   "the ring must hold a whole step group past any batch boundary");
     fpos = (fpos + W - 1) / W * W;
+#if QRMC_MMA_PIPE
+    // software pipeline: the shared-memory operands of chunk c+1 are loaded
+    // before the DMMAs of chunk c are issued, their products formed after
+    // (in-order issue: the loads' latency hides behind the tensor-core work)
+    {
+        double sa[RB], sb_[RB], b[NB];
+        uint32_t tp = __ldg(term);
+        ws.land(fpos + W);
+        {
+            const double* ps = trow + (tp & 0xFFFFu);
+            const double* pb = trow + (tp >> 16);
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                sa[r] = ps[8 * r];
+                sb_[r] = pb[8 * r];
+            }
+            const double* rb = ring + (fpos % kMmaRingFrags) * 32;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) b[i] = rb[32 * i];
+        }
+        for (int c = c0; c < c1; ++c) {
+            double a[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) a[r] = DMUL(sa[r], sb_[r]);
+            double bc[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) bc[i] = b[i];
+            // next chunk (the last iteration re-reads the current one)
+            const bool more = c + 1 < c1;
+            const uint32_t fn = more ? fpos + W : fpos;
+            if (more) {
+                term += 4;
+                ws.land(fn + W);
+            }
+            tp = __ldg(term);
+            {
+                const double* ps = trow + (tp & 0xFFFFu);
+                const double* pb = trow + (tp >> 16);
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    sa[r] = ps[8 * r];
+                    sb_[r] = pb[8 * r];
+                }
+                const double* rb = ring + (fn % kMmaRingFrags) * 32;
+#pragma unroll
+                for (int i = 0; i < NB; ++i) b[i] = rb[32 * i];
+            }
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+#pragma unroll
+                for (int r = 0; r < RB; ++r) dmma(acc[r][i], a[r], bc[i]);
+            fpos += W;
+            ws.refill(fpos);
+        }
+    }
+#else
     int c = c0;
 #if QRMC_MMA_UNROLL4
     for (; c + 3 < c1; c += 4) {
@@ -195,6 +254,7 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
         fpos += W;
         ws.refill(fpos);
     }
+#endif
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
 #pragma unroll
