@@ -552,6 +552,46 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
         if (cnt[static_cast<size_t>(pr)]) order.push_back(pr);
     std::stable_sort(order.begin(), order.end(),
                      [&](int32_t x, int32_t y) { return cnt[static_cast<size_t>(x)] > cnt[static_cast<size_t>(y)]; });
+    // Inside a layer of equal count the order is free: arrange each chunk of four
+    // terms so that their table rows of c_s and of c_b are distinct mod 4 -- the
+    // kernels read 4 terms x 4 paths per half-warp from [entry][path] tables with a
+    // row stride = 4 (mod 16) banks, so that makes both operand loads conflict-free.
+#ifndef QRMC_MMA_BANK_ORDER
+#define QRMC_MMA_BANK_ORDER 1
+#endif
+    if (QRMC_MMA_BANK_ORDER) {
+        std::vector<int32_t> out;
+        out.reserve(order.size());
+        size_t i = 0;
+        while (i < order.size()) {
+            size_t e = i;
+            while (e < order.size() && cnt[static_cast<size_t>(order[e])] == cnt[static_cast<size_t>(order[i])]) ++e;
+            std::vector<int32_t> pool(order.begin() + static_cast<std::ptrdiff_t>(i), order.begin() + static_cast<std::ptrdiff_t>(e));
+            while (!pool.empty()) {
+                // rows already in the current chunk
+                const size_t base = out.size() / 4 * 4;
+                unsigned used_s = 0, used_b = 0;
+                for (size_t q = base; q < out.size(); ++q) {
+                    used_s |= 1u << ((offset[d - 2] + out[q] / Bn) & 3);
+                    used_b |= 1u << ((offset[d - 1] + out[q] % Bn) & 3);
+                }
+                size_t best = 0;
+                int best_cost = 99;
+                for (size_t q = 0; q < pool.size() && best_cost > 0; ++q) {
+                    const int cs = (used_s >> ((offset[d - 2] + pool[q] / Bn) & 3)) & 1;
+                    const int cb = (used_b >> ((offset[d - 1] + pool[q] % Bn) & 3)) & 1;
+                    if (cs + cb < best_cost) {
+                        best_cost = cs + cb;
+                        best = q;
+                    }
+                }
+                out.push_back(pool[best]);
+                pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(best));
+            }
+            i = e;
+        }
+        order.swap(out);
+    }
     std::vector<int32_t> rank(static_cast<size_t>(S) * Bn, -1);
     for (size_t t = 0; t < order.size(); ++t) rank[static_cast<size_t>(order[t])] = static_cast<int32_t>(t);
     for (const Grp& gr : groups)
@@ -568,6 +608,39 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     std::vector<int32_t> gi(groups.size());
     for (size_t i = 0; i < gi.size(); ++i) gi[i] = static_cast<int32_t>(i);
     std::stable_sort(gi.begin(), gi.end(), [&](int32_t x, int32_t y) { return groups[x].n > groups[y].n; });
+    // Same freedom for groups of equal size: the K1 epilogue reads the prefix
+    // rows of groups n = 2 col + h (col = 0..3) of a column block per half-warp,
+    // so arrange each such quad to have distinct rows mod 4 on every level.
+    if (QRMC_MMA_BANK_ORDER) {
+        std::vector<int32_t> out;
+        out.reserve(gi.size());
+        size_t i = 0;
+        while (i < gi.size()) {
+            size_t e = i;
+            while (e < gi.size() && groups[gi[e]].n == groups[gi[i]].n) ++e;
+            std::vector<int32_t> pool(gi.begin() + static_cast<std::ptrdiff_t>(i), gi.begin() + static_cast<std::ptrdiff_t>(e));
+            while (!pool.empty()) {
+                const size_t pos = out.size(), blk = pos / 8 * 8;
+                std::vector<unsigned> used(static_cast<size_t>(nu), 0u);
+                for (size_t q = blk + pos % 2; q < pos; q += 2)
+                    for (int l = 0; l < nu; ++l) used[l] |= 1u << ((offset[l] + at(groups[out[q]].r0, l)) & 3);
+                size_t best = 0;
+                int best_cost = 1 << 20;
+                for (size_t q = 0; q < pool.size() && best_cost > 0; ++q) {
+                    int cost = 0;
+                    for (int l = 0; l < nu; ++l) cost += (used[l] >> ((offset[l] + at(groups[pool[q]].r0, l)) & 3)) & 1;
+                    if (cost < best_cost) {
+                        best_cost = cost;
+                        best = q;
+                    }
+                }
+                out.push_back(pool[best]);
+                pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(best));
+            }
+            i = e;
+        }
+        gi.swap(out);
+    }
     const int n_cb = static_cast<int>((gi.size() + 7) / 8);
     L.gk.assign(static_cast<size_t>(n_cb) * 8 * nu, 0);
     for (int c = 0; c < n_cb * 8; ++c)

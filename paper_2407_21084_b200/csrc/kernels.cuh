@@ -92,7 +92,10 @@ struct MmaArgs {
 // 4 paths); each warp keeps one rectangle of <= kProjTiles output tiles in
 // registers over all of the lane's paths.
 constexpr int kProjWarps = 16;
-constexpr int kProjTiles = 8;  // output tiles per warp: ng group blocks x nt term blocks, ng in {1,2,4,8}
+#ifndef QRMC_PROJ_TILES
+#define QRMC_PROJ_TILES 8
+#endif
+constexpr int kProjTiles = QRMC_PROJ_TILES;  // output tiles per warp: ng group blocks x nt term blocks, ng a power of 2
 constexpr int kProjBatch = 16;  // paths per shared-memory table batch (double-buffered)
 
 struct ProjMmaArgs {

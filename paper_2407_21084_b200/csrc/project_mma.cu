@@ -9,7 +9,7 @@
 //
 // is a GEMM [groups x paths] x [paths x terms] with a staircase N extent, run
 // as mma.sync.m8n8k4.f64 with M = 8 groups, N = 8 terms, K = 4 paths. Every
-// warp owns one rectangle of <= kProjRG x kProjRT output tiles (host.cpp
+// warp owns one rectangle of ng x nt <= kProjTiles output tiles (host.cpp
 // build_mma_layout) and keeps it in registers while the CTA streams the lane's
 // paths through shared memory in batches of kProjBatch: per batch, the cosine
 // tables c_k(x_l) of every coordinate are built once ([entry][path] layout as in
@@ -199,6 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, c
     // every warp runs the same batch loop (barriers included); the shape only
     // sets its register tile. Empty slots carry tiles = 0 and write nothing.
     switch (rc.z & 0xFF) {
+        case 16:
+            if constexpr (kProjTiles >= 16) project_rect<D, 16>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            break;
         case 8: project_rect<D, 8>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
         case 4: project_rect<D, 4>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
         case 2: project_rect<D, 2>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;

@@ -6,10 +6,8 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "b3w16": ("QRMC_MMA_BUNDLE=3", "QRMC_MMA_WARPS=16", "QRMC_MMA_UNROLL4=0"),
-    "b4w16": ("QRMC_MMA_BUNDLE=4", "QRMC_MMA_WARPS=16", "QRMC_MMA_UNROLL4=0"),
-    "b2w16": ("QRMC_MMA_WARPS=16",),
-    "b3w20": ("QRMC_MMA_BUNDLE=3", "QRMC_MMA_UNROLL4=0"),
+    "bank": (),
+    "nobank": ("QRMC_MMA_BANK_ORDER=0",),
 }
 def one(kv):
     name, defs = kv
