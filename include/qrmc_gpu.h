@@ -173,6 +173,13 @@ int64_t qrmc_gpu_plan_basis_size(const qrmc_gpu_plan_t* plan);
  * per_step (steps x 3, row i = cloud step i) or NULL. CUDA-event timed inside the graph. */
 qrmc_status qrmc_gpu_plan_kernel_seconds(const qrmc_gpu_plan_t* plan, double* out3, double* per_step,
                                          char* err, size_t err_len);
+/* table_to_json (proj/src/table_io.cpp:45-73): the reference's
+ * `qrmc.coefficients.v1` artifact, byte-identical, for `coeffs` (steps x K,
+ * row-major [i][k], Gamma order) solved with `config`. Host-only. Returns the
+ * length needed including the NUL (the text is written when out_len suffices),
+ * or -status on error. */
+int64_t qrmc_gpu_table_json(const qrmc_config_t* config, int32_t dim, double horizon, const double* coeffs,
+                            char* out, size_t out_len, char* err, size_t err_len);
 /* Host-only check of the tensor-core layout (no device needed): builds the
  * index set and the K1/K2 fragment layouts make_plan would use, replays both
  * kernels' data flow on the host for one random point and random coefficients,

@@ -191,6 +191,8 @@ def _declare(L: C.CDLL) -> None:
     L.qrmc_gpu_mma_layout_check.argtypes = [C.c_int32, C.c_int32, P(C.c_int32), C.c_int32, C.c_uint64,
                                             P(C.c_int64), P(C.c_double), cp, sz]
     L.qrmc_gpu_plan_kernel_name.argtypes = [vp, C.c_int]
+    L.qrmc_gpu_table_json.argtypes = [P(Config), C.c_int32, C.c_double, P(C.c_double), cp, sz, cp, sz]
+    L.qrmc_gpu_table_json.restype = C.c_int64
     L.qrmc_gpu_plan_kernel_name.restype = C.c_char_p
     L.qrmc_gpu_lane_ownership.argtypes = [C.c_int64, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32),
                                           P(C.c_int64)]
@@ -215,7 +217,7 @@ EXPORTED_SYMBOLS = (
     "qrmc_gpu_session_create", "qrmc_gpu_session_destroy", "qrmc_gpu_nccl_unique_id",
     "qrmc_gpu_backward_solve", "qrmc_gpu_plan_create", "qrmc_gpu_plan_run",
     "qrmc_gpu_plan_download", "qrmc_gpu_plan_basis_size", "qrmc_gpu_plan_stream",
-    "qrmc_gpu_plan_kernel_seconds", "qrmc_gpu_plan_io_bytes", "qrmc_gpu_plan_kernel_name", "qrmc_gpu_mma_layout_check", "qrmc_gpu_lane_ownership",
+    "qrmc_gpu_plan_kernel_seconds", "qrmc_gpu_plan_io_bytes", "qrmc_gpu_plan_kernel_name", "qrmc_gpu_mma_layout_check", "qrmc_gpu_table_json", "qrmc_gpu_lane_ownership",
     "qrmc_gpu_owned_path",
     "qrmc_gpu_plan_destroy", "qrmc_gpu_evaluate", "qrmc_gpu_mse_metrics", "qrmc_gpu_philox",
     "qrmc_gpu_stream_draws", "qrmc_gpu_cloud_paths",

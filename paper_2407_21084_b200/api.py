@@ -225,6 +225,76 @@ class CoefficientTable:
         raise_for(st, err.value.decode())
         return float(out[0]) if scalar else out
 
+    # ---- artifacts (proj/src/table_io.cpp) ----
+    def to_json(self) -> str:
+        """table_to_json (table_io.cpp:45-73): the `qrmc.coefficients.v1` document,
+        byte-identical to the reference's for the same table."""
+        cfg = self._config()
+        coeffs = np.ascontiguousarray(self.table, dtype=np.float64)
+        err = _err()
+        L = _abi.lib()
+        args = (cfg.ref(), self.gamma.dim, float(self.horizon), coeffs.ctypes.data_as(C.POINTER(C.c_double)))
+        n = L.qrmc_gpu_table_json(*args, None, 0, err, 1024)
+        if n < 0:
+            raise_for(int(-n), err.value.decode())
+        buf = C.create_string_buffer(int(n))
+        n = L.qrmc_gpu_table_json(*args, buf, int(n), err, 1024)
+        if n < 0:
+            raise_for(int(-n), err.value.decode())
+        return buf.value.decode()
+
+    def save_json(self, path) -> None:
+        """save_table_json (table_io.cpp:75-81): the document plus a newline."""
+        with open(path, "wb") as f:
+            f.write(self.to_json().encode() + b"\n")
+
+    @staticmethod
+    def from_json(text: str) -> "CoefficientTable":
+        """table_from_json (table_io.cpp:83-125): schema, step range, entry count and
+        index order are checked; IoError cases raise ValueError."""
+        import json
+
+        try:
+            doc = json.loads(text)
+        except ValueError as e:
+            raise ValueError(f"coefficient artifact: parse error: {e}") from e
+        try:
+            if doc["schema"] != "qrmc.coefficients.v1":
+                raise ValueError("coefficient artifact: unknown schema")
+            cfg = doc["config"]
+            m, g = cfg["measure"], cfg["gamma"]
+            measure = Measure(float(m["mu"]), int(m["dim"]), tuple(float(c) for c in m["center"]))
+            kind, dim, degrees = g["kind"], int(g["dim"]), tuple(int(v) for v in g["degrees"])
+            if kind == "full":
+                gamma = MultiIndexSet.full(degrees)
+            else:
+                if len(degrees) != 1:
+                    raise ValueError("gamma descriptor: total/hyperbolic take one degree")
+                gamma = MultiIndexSet(kind, dim, degrees)
+            rows = gamma.indices()
+            steps = int(cfg["steps"])
+            table = np.zeros((steps, rows.shape[0]))
+            for st in doc["coefficients"]:
+                i = int(st["step"])
+                if not (0 <= i < steps):
+                    raise ValueError("coefficient artifact: step index out of range")
+                entries = st["entries"]
+                if len(entries) != rows.shape[0]:
+                    raise ValueError("coefficient artifact: entry count != basis size")
+                for k, (idx, v) in enumerate(entries):
+                    if tuple(idx) != tuple(rows[k]):
+                        raise ValueError("coefficient artifact: index order mismatch")
+                    table[i, k] = float(v)
+            return CoefficientTable(steps, int(cfg["paths"]), float(cfg["damping"]), int(cfg["seed"]),
+                                    float(cfg["horizon"]), measure, gamma, table)
+        except (KeyError, TypeError) as e:
+            raise ValueError(f"coefficient artifact: malformed document: {e}") from e
+
+    @staticmethod
+    def load_json(path) -> "CoefficientTable":
+        with open(path, "rb") as f:
+            return CoefficientTable.from_json(f.read().decode())
+
 
 def backward_solve(problem: _abi.Problem, config: _abi.ConfigHolder, session=None):
     """qrmc::backward_solve (solver.hpp:91) through the C ABI.

@@ -20,10 +20,24 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libqrmc_gpu.so"
-SOURCES = [CSRC / "kernels.cu", CSRC / "responses_mma.cu", CSRC / "project_mma.cu", CSRC / "host.cpp"]
+SOURCES = [CSRC / "kernels.cu", CSRC / "responses_mma.cu", CSRC / "project_mma.cu", CSRC / "host.cpp",
+           CSRC / "table_io.cpp"]
 HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "series_block.cuh", CSRC / "mma_common.cuh", ROOT / "include" / "qrmc_gpu.h",
            ROOT / "include" / "qrmc_normal_quantile.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def json_include() -> str:
+    """nlohmann/json.hpp (the JSON library the reference builds against): the
+    coefficient artifact writer (csrc/table_io.cpp) serialises with it."""
+    import site
+    cands = [os.environ.get("QRMC_JSON_DIR", "")]
+    for p in site.getsitepackages():
+        cands.append(os.path.join(p, "include", "cudnn_frontend", "thirdparty", "nlohmann"))
+    for c in cands:
+        if c and Path(c, "json.hpp").exists():
+            return c
+    raise RuntimeError("nlohmann json.hpp not found (set QRMC_JSON_DIR)")
 
 
 def nvcc() -> str:
@@ -47,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
     target.parent.mkdir(parents=True, exist_ok=True)
     tmp = target.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}",
+           "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{json_include()}",
            *[f"-D{d}" for d in defines], *map(str, SOURCES), "-o", str(tmp), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
