@@ -6,8 +6,8 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "bank": (),
-    "nobank": ("QRMC_MMA_BANK_ORDER=0",),
+    "rb2w10": ("QRMC_MMA_RB=2", "QRMC_MMA_WARPS=10", "QRMC_MMA_MINB=2"),
+    "rb2w8": ("QRMC_MMA_RB=2", "QRMC_MMA_WARPS=8", "QRMC_MMA_MINB=2"),
 }
 def one(kv):
     name, defs = kv
