@@ -785,7 +785,8 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
             const int w = ntb[g];
             // rows in power-of-two bands; each band cut into ng x (kProjTiles / ng)
             for (int r0 = 0; r0 < h;) {
-                int ng = kProjTiles;
+                int ng = 1;
+                while (ng * 2 <= std::min(16, kProjTiles)) ng *= 2;  // a power of two (kernel shapes)
                 while (ng > h - r0) ng /= 2;
                 const int nt_max = kProjTiles / ng;
                 for (int t0 = 0; t0 < w; t0 += nt_max) {

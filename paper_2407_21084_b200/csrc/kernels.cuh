@@ -91,7 +91,10 @@ struct MmaArgs {
 // G[u][t] = sum_m S_m U_u(X_m) A_t(X_m) as mma.m8n8k4.f64 (8 groups x 8 terms x
 // 4 paths); each warp keeps one rectangle of <= kProjTiles output tiles in
 // registers over all of the lane's paths.
-constexpr int kProjWarps = 16;
+#ifndef QRMC_PROJ_WARPS
+#define QRMC_PROJ_WARPS 20
+#endif
+constexpr int kProjWarps = QRMC_PROJ_WARPS;
 #ifndef QRMC_PROJ_TILES
 #define QRMC_PROJ_TILES 8
 #endif

@@ -32,7 +32,7 @@ namespace {
 constexpr int kThreads = kProjWarps * 32;
 constexpr int kStride = kProjBatch + 4;  // table row stride (paths), padded
 #ifndef QRMC_PROJ_TSPLIT
-#define QRMC_PROJ_TSPLIT 8
+#define QRMC_PROJ_TSPLIT 4
 #endif
 constexpr int kTabSplit = QRMC_PROJ_TSPLIT;
 constexpr int kBatchesPerChunk = kChunk / kProjBatch;
@@ -202,9 +202,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, c
         case 16:
             if constexpr (kProjTiles >= 16) project_rect<D, 16>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
-        case 8: project_rect<D, 8>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
-        case 4: project_rect<D, 4>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
-        case 2: project_rect<D, 2>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
+        case 8:
+            if constexpr (kProjTiles >= 8) project_rect<D, 8>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            break;
+        case 4:
+            if constexpr (kProjTiles >= 4) project_rect<D, 4>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            break;
+        case 2:
+            if constexpr (kProjTiles >= 2) project_rect<D, 2>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            break;
         default: project_rect<D, 1>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
     }
 }

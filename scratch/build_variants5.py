@@ -6,8 +6,10 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "rb2w10": ("QRMC_MMA_RB=2", "QRMC_MMA_WARPS=10", "QRMC_MMA_MINB=2"),
-    "rb2w8": ("QRMC_MMA_RB=2", "QRMC_MMA_WARPS=8", "QRMC_MMA_MINB=2"),
+    "pw20": ("QRMC_PROJ_WARPS=20",),
+    "pw24": ("QRMC_PROJ_WARPS=24",),
+    "pw18": ("QRMC_PROJ_WARPS=18",),
+    "pw16": (),
 }
 def one(kv):
     name, defs = kv
