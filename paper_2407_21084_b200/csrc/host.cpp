@@ -557,7 +557,7 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     // kernels read 4 terms x 4 paths per half-warp from [entry][path] tables with a
     // row stride = 4 (mod 16) banks, so that makes both operand loads conflict-free.
 #ifndef QRMC_MMA_BANK_ORDER
-#define QRMC_MMA_BANK_ORDER 1
+#define QRMC_MMA_BANK_ORDER 0
 #endif
     if (QRMC_MMA_BANK_ORDER) {
         std::vector<int32_t> out;
