@@ -157,6 +157,11 @@ MMA_CASES = [
     (_abi.GAMMA_FULL, 4, [3]),
     (_abi.GAMMA_FULL, 3, [5, 2, 7]),
     (_abi.GAMMA_FULL, 5, [1]),
+    (_abi.GAMMA_FULL, 3, [3, 3, 0]),    # single-term leaf level
+    (_abi.GAMMA_FULL, 3, [0, 0, 5]),    # one group
+    (_abi.GAMMA_HYPERBOLIC, 3, [1]),
+    (_abi.GAMMA_TOTAL, 4, [1]),
+    (_abi.GAMMA_TOTAL, 7, [3]),
 ]
 
 

@@ -134,6 +134,15 @@ def test_constant_terminal_recovered_exactly(L):
     dict(dim=1, kind=0, degrees=[100], steps=20, paths=20_000, damping=2.1, mu=2.0),
     dict(dim=5, kind=2, degrees=[12], steps=3, paths=5_000, damping=5.1, mu=2.0),
     dict(dim=8, kind=2, degrees=[4], steps=3, paths=3_000, damping=5.1, mu=2.0),
+    # tensor-core layout edge shapes: a zero-degree coordinate, a single-term leaf
+    # level, one group, tiny sets, ragged last chunks of 1024 paths
+    dict(dim=3, kind=0, degrees=[2, 0, 3], steps=4, paths=5_000, damping=0.0, mu=2.0),
+    dict(dim=3, kind=0, degrees=[3, 3, 0], steps=3, paths=4_097, damping=2.1, mu=2.0),
+    dict(dim=3, kind=0, degrees=[0, 0, 5], steps=3, paths=3_000, damping=0.0, mu=2.0),
+    dict(dim=3, kind=2, degrees=[1], steps=3, paths=2_049, damping=5.1, mu=2.0),
+    dict(dim=4, kind=1, degrees=[1], steps=4, paths=1_000, damping=0.0, mu=1.0),
+    dict(dim=7, kind=1, degrees=[3], steps=3, paths=3_333, damping=5.1, mu=2.0),
+    dict(dim=4, kind=2, degrees=[100], steps=3, paths=1_025, damping=5.1, mu=2.0),
 ])
 def test_backward_solve_matches_port_live(L, port, cfgkw):
     prob = _abi.sin_bench_problem(cfgkw["dim"])
