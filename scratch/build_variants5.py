@@ -6,11 +6,8 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "w20pt6": ("QRMC_PROJ_TILES=6",),
-    "w20pt10": ("QRMC_PROJ_TILES=10",),
-    "w20t2": ("QRMC_PROJ_TSPLIT=2",),
-    "w20t8": ("QRMC_PROJ_TSPLIT=8",),
-    "w20": (),
+    "nors": ("QRMC_MMA_REFILL_SYNC=0",),
+    "rs": (),
 }
 def one(kv):
     name, defs = kv
