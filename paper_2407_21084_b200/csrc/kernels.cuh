@@ -60,10 +60,10 @@ constexpr int kMmaPaths = 8 * kMmaRowBlocks;     // paths per CTA
 #define QRMC_MMA_BUNDLE 2
 #endif
 #ifndef QRMC_MMA_BATCH
-#define QRMC_MMA_BATCH 4
+#define QRMC_MMA_BATCH 8
 #endif
 #ifndef QRMC_MMA_RING
-#define QRMC_MMA_RING 4
+#define QRMC_MMA_RING 2
 #endif
 constexpr int kMmaBundle = QRMC_MMA_BUNDLE;      // max column blocks per unit (1..4)
 constexpr int kMmaBatch = QRMC_MMA_BATCH;        // fragments per copy batch (256 B each)

@@ -99,31 +99,38 @@ struct WarpStream {
     uint32_t issued, landed;
     uint32_t ready;     // fragments landed: landed * kMmaBatch
     uint32_t refill_at; // stream position that frees the next slot
+    uint32_t b_in;      // next batch's index inside its series
+    const double* next; // next batch's source
     int lane;
 
     __device__ __forceinline__ void issue() {
-        const uint32_t s = issued / per, b = issued - s * per;
-        const double* g = src + s * row_len + static_cast<int64_t>(b) * (kMmaBatch * 32);
         double* d = ring + (issued % kMmaRingBatches) * (kMmaBatch * 32);
 #pragma unroll
-        for (int c = 0; c < kMmaBatch * 32 / 2 / 32; ++c) cp_async16(d + 2 * (c * 32 + lane), g + 2 * (c * 32 + lane));
+        for (int c = 0; c < kMmaBatch * 32 / 2 / 32; ++c)
+            cp_async16(d + 2 * (c * 32 + lane), next + 2 * (c * 32 + lane));
         cp_async_commit();
         ++issued;
         refill_at += kMmaBatch;
+        next += kMmaBatch * 32;
+        if (++b_in == per) {  // next series: alpha_{j+2} of the same warp's stream
+            b_in = 0;
+            src += row_len;
+            next = src;
+        }
     }
     // make fragments [.., upto) visible to the whole warp
     __device__ __forceinline__ void land(uint32_t upto) {
         if (upto <= ready) return;
-        do {
-            switch (issued - landed - 1) {
-                case 0: cp_async_wait<0>(); break;
-                case 1: cp_async_wait<1>(); break;
-                case 2: cp_async_wait<2>(); break;
-                default: cp_async_wait<3>(); break;
-            }
-            ++landed;
-            ready += kMmaBatch;
-        } while (upto > ready);
+        // batches [0, need) must have landed: allow issued - need to stay in flight
+        const uint32_t need = (upto + kMmaBatch - 1) / kMmaBatch;
+        switch (issued - need) {
+            case 0: cp_async_wait<0>(); break;
+            case 1: cp_async_wait<1>(); break;
+            case 2: cp_async_wait<2>(); break;
+            default: cp_async_wait<3>(); break;
+        }
+        landed = need;
+        ready = need * kMmaBatch;
         __syncwarp();
     }
     // fragments below `consumed` are read: refill the freed slots
@@ -307,6 +314,8 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
     ws.landed = 0;
     ws.ready = 0;
     ws.refill_at = 0;
+    ws.b_in = 0;
+    ws.next = ws.src;
     ws.lane = lane;
     while (ws.issued < ws.total && ws.issued < kMmaRingBatches) ws.issue();
     ws.refill_at = kMmaBatch;  // batch kMmaRingBatches reuses the first slot
