@@ -15,6 +15,13 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// D = A B (accumulator start: C = 0)
+__device__ __forceinline__ void dmma0(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+        : "=d"(c[0]), "=d"(c[1])
+        : "d"(a), "d"(b), "d"(0.0), "d"(0.0));
+}
+
 // u64 draw number idx of a stream (RngStream order: two draws per Philox block,
 // low half first; rng.hpp:60-75), without walking the stream.
 __device__ __forceinline__ uint64_t stream_u64_at(uint64_t seed, uint64_t sid, uint64_t idx) {

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -55,9 +56,6 @@ __device__ __forceinline__ long long sync_clk() {
 }
 #ifndef QRMC_MMA_AHEAD
 #define QRMC_MMA_AHEAD 2
-#endif
-#ifndef QRMC_MMA_PIPE
-#define QRMC_MMA_PIPE 0
 #endif
 #ifndef QRMC_MMA_UNROLL4
 #define QRMC_MMA_UNROLL4 1
@@ -151,15 +149,11 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
                                          const double* tab, int lane, double (&y)[kMmaRowBlocks]) {
     constexpr int RB = kMmaRowBlocks;
     const int row = lane >> 2, col = lane & 3;
-    double acc[RB][NB][2];
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-#pragma unroll
-        for (int i = 0; i < NB; ++i) acc[r][i][0] = acc[r][i][1] = 0.0;
+    double acc[RB][NB][2];  // written first by the unit's first chunk (C = 0)
     const double* trow = tab + row;
     const double* ring = ws.ring + lane;
     const uint32_t* term = m.terms + 4 * c0 + col;
-    auto step = [&](uint32_t f) {
+    auto step = [&](auto first, uint32_t f) {
         const uint32_t tp = __ldg(term);
         term += 4;
         const double* ps = trow + (tp & 0xFFFFu);
@@ -174,94 +168,47 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
 #pragma unroll
         for (int i = 0; i < NB; ++i)
 #pragma unroll
-            for (int r = 0; r < RB; ++r) dmma(acc[r][i], a[r], b[i]);
+            for (int r = 0; r < RB; ++r) {
+                if constexpr (decltype(first)::value)
+                    dmma0(acc[r][i], a[r], b[i]);
+                else
+                    dmma(acc[r][i], a[r], b[i]);
+            }
     };
     constexpr uint32_t W = NB == 3 ? 4 : NB;  // fragment slots per step (host.cpp build_mma_layout)
     static_assert((QRMC_MMA_UNROLL4 ? 4 : 2) * W + kMmaBatch - 1 <= kMmaRingFrags,
                   "the ring must hold a whole step group past any batch boundary");
     fpos = (fpos + W - 1) / W * W;
-#if QRMC_MMA_PIPE
-    // software pipeline: the shared-memory operands of chunk c+1 are loaded
-    // before the DMMAs of chunk c are issued, their products formed after
-    // (in-order issue: the loads' latency hides behind the tensor-core work)
-    {
-        double sa[RB], sb_[RB], b[NB];
-        uint32_t tp = __ldg(term);
-        ws.land(fpos + W);
-        {
-            const double* ps = trow + (tp & 0xFFFFu);
-            const double* pb = trow + (tp >> 16);
-#pragma unroll
-            for (int r = 0; r < RB; ++r) {
-                sa[r] = ps[8 * r];
-                sb_[r] = pb[8 * r];
-            }
-            const double* rb = ring + (fpos % kMmaRingFrags) * 32;
-#pragma unroll
-            for (int i = 0; i < NB; ++i) b[i] = rb[32 * i];
-        }
-        for (int c = c0; c < c1; ++c) {
-            double a[RB];
-#pragma unroll
-            for (int r = 0; r < RB; ++r) a[r] = DMUL(sa[r], sb_[r]);
-            double bc[NB];
-#pragma unroll
-            for (int i = 0; i < NB; ++i) bc[i] = b[i];
-            // next chunk (the last iteration re-reads the current one)
-            const bool more = c + 1 < c1;
-            const uint32_t fn = more ? fpos + W : fpos;
-            if (more) {
-                term += 4;
-                ws.land(fn + W);
-            }
-            tp = __ldg(term);
-            {
-                const double* ps = trow + (tp & 0xFFFFu);
-                const double* pb = trow + (tp >> 16);
-#pragma unroll
-                for (int r = 0; r < RB; ++r) {
-                    sa[r] = ps[8 * r];
-                    sb_[r] = pb[8 * r];
-                }
-                const double* rb = ring + (fn % kMmaRingFrags) * 32;
-#pragma unroll
-                for (int i = 0; i < NB; ++i) b[i] = rb[32 * i];
-            }
-#pragma unroll
-            for (int i = 0; i < NB; ++i)
-#pragma unroll
-                for (int r = 0; r < RB; ++r) dmma(acc[r][i], a[r], bc[i]);
-            fpos += W;
-            ws.refill(fpos);
-        }
-    }
-#else
-    int c = c0;
+    // the first chunk starts the accumulators
+    ws.land(fpos + W);
+    step(std::true_type{}, fpos);
+    fpos += W;
+    ws.refill(fpos);
+    int c = c0 + 1;
 #if QRMC_MMA_UNROLL4
     for (; c + 3 < c1; c += 4) {
         ws.land(fpos + 4 * W);
-        step(fpos);
-        step(fpos + W);
-        step(fpos + 2 * W);
-        step(fpos + 3 * W);
+        step(std::false_type{}, fpos);
+        step(std::false_type{}, fpos + W);
+        step(std::false_type{}, fpos + 2 * W);
+        step(std::false_type{}, fpos + 3 * W);
         fpos += 4 * W;
         ws.refill(fpos);
     }
 #endif
     for (; c + 1 < c1; c += 2) {
         ws.land(fpos + 2 * W);
-        step(fpos);
-        step(fpos + W);
+        step(std::false_type{}, fpos);
+        step(std::false_type{}, fpos + W);
         fpos += 2 * W;
         ws.refill(fpos);
     }
     if (c < c1) {
         ws.land(fpos + W);
-        step(fpos);
+        step(std::false_type{}, fpos);
         fpos += W;
         ws.refill(fpos);
     }
-#endif
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
 #pragma unroll

@@ -6,9 +6,7 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "b8r2": ("QRMC_MMA_BATCH=8", "QRMC_MMA_RING=2"),
-    "b4r4": (),
-    "b2r8": ("QRMC_MMA_BATCH=2", "QRMC_MMA_RING=8", "QRMC_MMA_UNROLL4=0"),
+    "k2nt": (),
 }
 def one(kv):
     name, defs = kv
