@@ -211,12 +211,21 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
     }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
+        // the lane's two groups g, g+1 (g even) have adjacent prefix rows:
+        // 2 (D-2) u16 = (D-2) aligned u32 words
+        const int g0 = 8 * (cb0 + i) + 2 * col;
+        uint32_t wpair[D - 2];
+        const uint32_t* gw = reinterpret_cast<const uint32_t*>(m.gk + g0 * (D - 2));
+#pragma unroll
+        for (int w = 0; w < D - 2; ++w) wpair[w] = __ldg(gw + w);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int g = 8 * (cb0 + i) + 2 * col + h;
             const double* pu[D - 2];
 #pragma unroll
-            for (int l = 0; l < D - 2; ++l) pu[l] = trow + __ldg(&m.gk[g * (D - 2) + l]);
+            for (int l = 0; l < D - 2; ++l) {
+                const int e = h * (D - 2) + l;  // u16 entry of the pair
+                pu[l] = trow + ((wpair[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+            }
 #pragma unroll
             for (int r = 0; r < RB; ++r) {
                 double u = pu[0][8 * r];

@@ -6,7 +6,7 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "k2nt": (),
+    "gk32": (),
 }
 def one(kv):
     name, defs = kv
