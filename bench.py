@@ -262,8 +262,9 @@ def run_ours(args) -> int:
     value = path_steps(paths_total, n) / per_solve
     launches = int(stats.kernel_launches) * args.steps
 
-    # roofline of the dominant kernel, k_responses (phase 1): 2 FLOPs per basis term per
-    # future-point evaluation, M_local * sum_i (N-1-i) evaluations per solve.
+    # roofline of the dominant kernel, phase 1 (k_responses_mma on the FP64 tensor cores
+    # for this workload): 2 FLOPs per basis term per future-point evaluation,
+    # M_local * sum_i (N-1-i) evaluations per solve, against the measured DMMA peak.
     m_local = args.paths
     resp_flops = 2.0 * K * m_local * n * (n - 1) / 2.0
     resp_s = kernel_s[0] / args.steps
