@@ -291,3 +291,12 @@ def test_tensor_core_and_series_kernels_agree(L):
         del os.environ["QRMC_K2"]
     assert alpha_close(a, b) <= ALPHA_TOL
     assert (sa.applications, sa.clipped) == (sb.applications, sb.clipped)
+
+
+def test_tensor_core_kernels_fall_back_when_tables_exceed_smem(L):
+    # per-path cosine tables of 2 x 601 + 3 entries do not fit shared memory with 32
+    # paths: the plan takes the series-program kernels (still no CPU fallback)
+    prob = _abi.sin_bench_problem(3)
+    cfg = _abi.ConfigHolder(steps=2, paths=1024, damping=0.0, seed=1, gamma_kind=_abi.GAMMA_FULL,
+                            degrees=[600, 600, 2])
+    assert _kernel_names(prob, cfg)[:2] == ["k_responses", "k_project"]
