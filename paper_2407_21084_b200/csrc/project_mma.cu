@@ -31,6 +31,9 @@ namespace {
 
 constexpr int kThreads = kProjWarps * 32;
 constexpr int kStride = kProjBatch + 4;  // table row stride (paths), padded
+#ifndef QRMC_PROJ_BRANCHLESS
+#define QRMC_PROJ_BRANCHLESS 1
+#endif
 #ifndef QRMC_PROJ_TSPLIT
 #define QRMC_PROJ_TSPLIT 4
 #endif
@@ -156,6 +159,17 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
                 for (int l = 1; l < D - 2; ++l) u = DMUL(u, tm[gro[ig][l]]);
                 w[ig] = u;
             }
+#if QRMC_PROJ_BRANCHLESS
+            // every tile of the shape runs (tiles past nt read row 0 and are never
+            // written out): no data-dependent branch around mma.sync, so no
+            // warp re-convergence before each DMMA
+#pragma unroll
+            for (int it = 0; it < NT; ++it) {
+                const double bv = DMUL(tm[ts_[it]], tm[tb_[it]]);
+#pragma unroll
+                for (int ig = 0; ig < NG; ++ig) dmma(acc[ig][it], w[ig], bv);
+            }
+#else
 #pragma unroll
             for (int it = 0; it < NT; ++it) {
                 if (NT == 1 || it < nt) {
@@ -164,6 +178,7 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
                     for (int ig = 0; ig < NG; ++ig) dmma(acc[ig][it], w[ig], bv);
                 }
             }
+#endif
         }
         __syncthreads();
     }

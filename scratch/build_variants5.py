@@ -6,7 +6,8 @@ sys.path.insert(0, ".")
 from paper_2407_21084_b200 import build
 base = ("QRMC_ONLY_DIM=4",)
 V = {
-    "gk32": (),
+    "k2bl": (),
+    "k2br": ("QRMC_PROJ_BRANCHLESS=0",),
 }
 def one(kv):
     name, defs = kv
