@@ -54,7 +54,37 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS + [Path(__file__)])
 
 
+SRMC_OUT = PKG / "_lib" / "libqrmc_srmc.so"
+SRMC_SOURCES = [CSRC / "srmc.cu"]
+SRMC_HEADERS = [CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", ROOT / "include" / "qrmc_srmc.h",
+                ROOT / "include" / "qrmc_gpu.h", ROOT / "include" / "qrmc_normal_quantile.h"]
+
+
+def build_srmc(force: bool = False, verbose: bool = False) -> Path:
+    """Second in-tree library: the SRMC solver (include/qrmc_srmc.h)."""
+    if not force and SRMC_OUT.exists():
+        t = SRMC_OUT.stat().st_mtime
+        if all(p.stat().st_mtime <= t for p in SRMC_SOURCES + SRMC_HEADERS + [Path(__file__)]):
+            return SRMC_OUT
+    SRMC_OUT.parent.mkdir(parents=True, exist_ok=True)
+    tmp = SRMC_OUT.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler",
+           "-fPIC", "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}", *map(str, SRMC_SOURCES), "-o",
+           str(tmp)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr}")
+    if verbose and r.stderr:
+        print(r.stderr, file=sys.stderr)
+    tmp.replace(SRMC_OUT)
+    return SRMC_OUT
+
+
 def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    if out is None:
+        build_srmc(force=force, verbose=verbose)
     target = out or OUT
     if out is None and not force and not needs_build():
         return OUT

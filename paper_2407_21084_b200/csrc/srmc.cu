@@ -1,0 +1,516 @@
+// srmc.cu -- stratified regression Monte Carlo on sm_100a.
+//
+// The scheme, tables and C ABI are specified in include/qrmc_srmc.h. One warp owns one
+// hypercube of one backward step: its 32 lanes draw the cell's M paths (counter-based
+// Philox keyed by (seed; step, cell*M + path) -- rng.hpp:26-65 with the cell folded into
+// the path counter), take the Euler step (sde.cpp:37-73), gather the next step's local
+// polynomial of the cell the endpoint lands in (P doubles, read-only path), apply the
+// driver functor and accumulate the cell's normal equations in registers. A butterfly of
+// warp shuffles reduces them and every lane solves the P x P system (Cholesky, FP64,
+// registers). Paths never touch HBM; per step the only traffic is the gather of the
+// step-(i+1) table (L2-resident neighbourhoods: one Euler step moves ~sqrt(dt) << h)
+// and the write of the step-i table. When the driver reads z (Bergman) the warp runs
+// the cell twice: pass 1 fits Z, pass 2 replays the SAME draws (counter-based stream, no
+// storage) and fits Y with f(t_{i+1}, X_{i+1}, Y1, Zhat_i(X_i)).
+//
+// Replay-critical arithmetic (starts, Euler, cell index) is spelled with _rn intrinsics
+// so it matches oracle/srmc_oracle.c (built with -ffp-contract=off) bit for bit; the
+// reduction order differs (per-lane strided partials + butterfly), covered by the
+// stated tolerance (tests/test_srmc.py).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "qrmc_device.cuh"
+#include "qrmc_srmc.h"
+
+namespace {
+
+using namespace qrmc_dev;
+
+struct SrmcDev {
+    int kind, n, step, last;
+    int64_t cells, M;
+    uint64_t seed;
+    double lo, hi, h, inv2h, dt, sqrt_dt, t, T, L;
+    double p[8];
+    double bdt, sig;  // Euler: x + bdt + sig * sqrt_dt * z
+};
+
+template <int D>
+__device__ __forceinline__ double srmc_terminal(const SrmcDev& s, const double* x) {
+    double sum = 0.0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) sum = DADD(sum, x[l]);
+    if (s.kind == QRMC_SRMC_SIN_BENCH) return DADD(DADD(1.0, s.p[0]), sin(DMUL(s.p[1], sum)));
+    const double v = DSUB(exp(DDIV(sum, static_cast<double>(D))), s.p[4]);
+    return v > 0.0 ? v : 0.0;
+}
+
+// driver f(t, x, y, z): SinBenchmark (benchmark.cpp:46-62, no z) or Bergman.
+template <int D>
+__device__ __forceinline__ double srmc_driver(const SrmcDev& s, const double* x, double y, const double* z) {
+    if (s.kind == QRMC_SRMC_SIN_BENCH) {
+        double sum = 0.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) sum = DADD(sum, x[l]);
+        const double lam = s.p[1];
+        const double e = exp(DDIV(DMUL(DMUL(DMUL(lam, lam), static_cast<double>(D)), DSUB(s.t, s.T)), 2.0));
+        const double w = DSUB(DSUB(DSUB(y, s.p[0]), 1.0), DMUL(sin(DMUL(lam, sum)), e));
+        const double ww = DMUL(w, w);
+        return ww < 1.0 ? ww : 1.0;
+    }
+    const double mu = s.p[0], sg = s.p[1], rl = s.p[2], rb = s.p[3];
+    double zs = 0.0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) zs = DADD(zs, z[l]);
+    const double theta = DDIV(DSUB(mu, rl), sg);
+    const double borrow = DSUB(DDIV(zs, sg), y);
+    return DADD(DSUB(DMUL(-rl, y), DMUL(theta, zs)), DMUL(DSUB(rb, rl), borrow > 0.0 ? borrow : 0.0));
+}
+
+// yhat_{i+1}(x): projection onto the box, cell index (bit-exact), local polynomial.
+template <int D, int P>
+__device__ __forceinline__ double srmc_eval(const SrmcDev& s, const double* __restrict__ tab, const double* x) {
+    int64_t k = 0;
+    double sl[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        double xc = x[l] < s.lo ? s.lo : x[l];
+        xc = xc > s.hi ? s.hi : xc;
+        int c = static_cast<int>(floor(DDIV(DSUB(xc, s.lo), s.h)));
+        c = c < 0 ? 0 : (c >= s.n ? s.n - 1 : c);
+        k = k * s.n + c;
+        const double centre = DADD(s.lo, DMUL(DADD(static_cast<double>(c), 0.5), s.h));
+        sl[l] = DMUL(DSUB(xc, centre), s.inv2h);
+    }
+    const double* row = tab + k * P;
+    double v = __ldg(row);
+    if constexpr (P > 1) {
+#pragma unroll
+        for (int l = 0; l < D; ++l) v = fma(__ldg(row + 1 + l), sl[l], v);
+    }
+    return v;
+}
+
+template <int NV>
+__device__ __forceinline__ void warp_sum(double* a) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a[j] += __shfl_xor_sync(0xffffffffu, a[j], o);
+    }
+}
+
+// Cholesky solve of the P x P normal equations (packed upper triangle A, row-major
+// a(r,c) r <= c) for nr right-hand sides b[nr][P]; a zero/negative pivot zeroes that
+// coefficient (degenerate cell: fewer distinct points than unknowns).
+template <int P, int NR>
+__device__ __forceinline__ void chol_solve(const double* A, double* b) {
+    double Lm[P][P];
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+        for (int c = 0; c < P; ++c) Lm[r][c] = 0.0;
+    int idx = 0;
+    double a[P][P];
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+        for (int c = r; c < P; ++c) {
+            a[r][c] = A[idx];
+            a[c][r] = A[idx];
+            ++idx;
+        }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        double d = a[j][j];
+#pragma unroll
+        for (int q = 0; q < j; ++q) d -= Lm[j][q] * Lm[j][q];
+        const double ljj = d > 1e-300 ? sqrt(d) : 0.0;
+        Lm[j][j] = ljj;
+#pragma unroll
+        for (int r = j + 1; r < P; ++r) {
+            double v = a[r][j];
+#pragma unroll
+            for (int q = 0; q < j; ++q) v -= Lm[r][q] * Lm[j][q];
+            Lm[r][j] = ljj > 0.0 ? v / ljj : 0.0;
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < NR; ++h) {
+        double* y = b + h * P;
+#pragma unroll
+        for (int r = 0; r < P; ++r) {
+            double v = y[r];
+#pragma unroll
+            for (int q = 0; q < r; ++q) v -= Lm[r][q] * y[q];
+            y[r] = Lm[r][r] > 0.0 ? v / Lm[r][r] : 0.0;
+        }
+#pragma unroll
+        for (int r = P - 1; r >= 0; --r) {
+            double v = y[r];
+#pragma unroll
+            for (int q = r + 1; q < P; ++q) v -= Lm[q][r] * y[q];
+            y[r] = Lm[r][r] > 0.0 ? v / Lm[r][r] : 0.0;
+        }
+    }
+}
+
+// One path of cell k: start X_i (and its local coordinates), dW, endpoint response Y1.
+template <int D, int P>
+__device__ __forceinline__ void srmc_path(const SrmcDev& s, const double* __restrict__ next, const int* cc,
+                                          int64_t k, int64_t m, double* x0, double* sl, double* dw, double* x1, double& y1) {
+    Stream rng(s.seed, sid_training(s.step, static_cast<uint64_t>(k) * static_cast<uint64_t>(s.M) + m));
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        const double u = rng.next_uniform();
+        x0[l] = DADD(s.lo, DMUL(DADD(static_cast<double>(cc[l]), u), s.h));
+        sl[l] = DSUB(DMUL(2.0, u), 1.0);
+    }
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        dw[l] = DMUL(s.sqrt_dt, rng.next_normal());
+        x1[l] = DADD(DADD(x0[l], s.bdt), DMUL(s.sig, dw[l]));
+    }
+    if (s.last) {
+        y1 = srmc_terminal<D>(s, x1);
+    } else {
+        y1 = srmc_eval<D, P>(s, next, x1);
+        y1 = y1 < -s.L ? -s.L : (y1 > s.L ? s.L : y1);
+    }
+}
+
+template <int D, int P>
+__device__ __forceinline__ void phi_of(const double* sl, double* phi) {
+    phi[0] = 1.0;
+#pragma unroll
+    for (int l = 0; l + 1 < P; ++l) phi[1 + l] = sl[l];
+}
+
+template <int D, int P>
+__device__ __forceinline__ void acc_gram(double* A, const double* phi) {
+    int idx = 0;
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+        for (int c = r; c < P; ++c) A[idx++] += phi[r] * phi[c];
+}
+
+// ZPASS: the driver reads z -> pass 1 fits Z, pass 2 replays and fits Y.
+// WANTZ: fit Z alongside Y in a single pass (driver without z).
+template <int D, int P, bool ZPASS, bool WANTZ>
+__global__ void __launch_bounds__(256) k_srmc_step(SrmcDev s, const double* __restrict__ next,
+                                                   double* __restrict__ ytab, double* __restrict__ ztab) {
+    constexpr int NA = P * (P + 1) / 2;
+    constexpr bool ANYZ = ZPASS || WANTZ;
+    const int lane = threadIdx.x & 31;
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (k >= s.cells) return;  // whole warps exit together
+    int cc[D];
+    {
+        int64_t r = k;
+#pragma unroll
+        for (int l = D - 1; l >= 0; --l) {
+            cc[l] = static_cast<int>(r % s.n);
+            r /= s.n;
+        }
+    }
+    double A[NA];
+    double by[P];
+    double bz[ANYZ ? D * P : 1];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) A[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) by[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < (ANYZ ? D * P : 1); ++j) bz[j] = 0.0;
+
+    double x0[D], sl[D], dw[D], x1[D], phi[P], y1;
+    const double zero_z[D] = {};
+    for (int64_t m = lane; m < s.M; m += 32) {
+        srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1);
+        phi_of<D, P>(sl, phi);
+        acc_gram<D, P>(A, phi);
+        if constexpr (ANYZ) {
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                const double rz = DDIV(DMUL(y1, dw[l]), s.dt);
+#pragma unroll
+                for (int p = 0; p < P; ++p) bz[l * P + p] += rz * phi[p];
+            }
+        }
+        if constexpr (!ZPASS) {
+            const double ry = DADD(y1, DMUL(s.dt, srmc_driver<D>(s, x1, y1, zero_z)));
+#pragma unroll
+            for (int p = 0; p < P; ++p) by[p] += ry * phi[p];
+        }
+    }
+    warp_sum<NA>(A);
+    if constexpr (ANYZ) {
+        warp_sum<D * P>(bz);
+        chol_solve<P, D>(A, bz);
+    }
+    if constexpr (ZPASS) {
+        for (int64_t m = lane; m < s.M; m += 32) {
+            srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1);
+            phi_of<D, P>(sl, phi);
+            double zi[D];
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                double v = bz[l * P];
+#pragma unroll
+                for (int p = 1; p < P; ++p) v = fma(bz[l * P + p], phi[p], v);
+                zi[l] = v;
+            }
+            const double ry = DADD(y1, DMUL(s.dt, srmc_driver<D>(s, x1, y1, zi)));
+#pragma unroll
+            for (int p = 0; p < P; ++p) by[p] += ry * phi[p];
+        }
+    }
+    warp_sum<P>(by);
+    chol_solve<P, 1>(A, by);
+    if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) ytab[k * P + p] = by[p];
+        if constexpr (ANYZ) {
+#pragma unroll
+            for (int j = 0; j < D * P; ++j) ztab[k * D * P + j] = bz[j];
+        }
+    }
+}
+
+template <int D, int P>
+__global__ void k_srmc_eval(SrmcDev s, const double* __restrict__ tab, const double* __restrict__ x, int64_t n,
+                            double* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double xi[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) xi[l] = x[i * D + l];
+    out[i] = srmc_eval<D, P>(s, tab, xi);
+}
+
+void set_err(char* err, size_t len, const char* msg) {
+    if (err && len) {
+        std::strncpy(err, msg, len - 1);
+        err[len - 1] = '\0';
+    }
+}
+
+bool needs_z(const qrmc_srmc_problem_t* p) { return p->kind == QRMC_SRMC_BERGMAN; }
+
+int validate(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c, char* err, size_t el) {
+    if (!p || !c) return set_err(err, el, "null problem/config"), QRMC_EINVAL;
+    if (p->kind != QRMC_SRMC_SIN_BENCH && p->kind != QRMC_SRMC_BERGMAN)
+        return set_err(err, el, "unknown SRMC problem kind"), QRMC_ENOTIMPL;
+    if (p->dim < 1 || p->dim > 6) return set_err(err, el, "SRMC dim must be in [1, 6]"), QRMC_EINVAL;
+    if (!(p->horizon > 0.0)) return set_err(err, el, "horizon must be > 0"), QRMC_EINVAL;
+    if (c->steps < 1) return set_err(err, el, "steps must be >= 1"), QRMC_EINVAL;
+    if (c->cells_per_dim < 1) return set_err(err, el, "cells_per_dim must be >= 1"), QRMC_EINVAL;
+    if (c->basis != QRMC_SRMC_LP0 && c->basis != QRMC_SRMC_LP1)
+        return set_err(err, el, "basis must be LP0 or LP1"), QRMC_EINVAL;
+    if (!(c->hi > c->lo)) return set_err(err, el, "domain needs hi > lo"), QRMC_EINVAL;
+    if (!(c->truncation > 0.0)) return set_err(err, el, "truncation must be > 0"), QRMC_EINVAL;
+    const int P = c->basis == QRMC_SRMC_LP1 ? p->dim + 1 : 1;
+    if (c->paths_per_cell < P) return set_err(err, el, "paths_per_cell must be >= basis size"), QRMC_EINVAL;
+    double cells = std::pow(static_cast<double>(c->cells_per_dim), p->dim);
+    if (cells * static_cast<double>(c->paths_per_cell) >= 0x1p40)
+        return set_err(err, el, "cells * paths_per_cell must be < 2^40 (stream id path field)"), QRMC_ECAPACITY;
+    return QRMC_OK;
+}
+
+SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
+    SrmcDev s{};
+    s.kind = p->kind;
+    s.n = c->cells_per_dim;
+    s.cells = 1;
+    for (int l = 0; l < p->dim; ++l) s.cells *= c->cells_per_dim;
+    s.M = c->paths_per_cell;
+    s.seed = c->seed;
+    s.lo = c->lo;
+    s.hi = c->hi;
+    s.h = (c->hi - c->lo) / c->cells_per_dim;
+    s.inv2h = 2.0 / s.h;
+    s.T = p->horizon;
+    s.dt = p->horizon / c->steps;
+    s.sqrt_dt = std::sqrt(s.dt);
+    s.L = c->truncation;
+    for (int j = 0; j < 8; ++j) s.p[j] = p->params[j];
+    if (p->kind == QRMC_SRMC_BERGMAN) {
+        volatile double drift = p->params[0] - 0.5 * (p->params[1] * p->params[1]);
+        s.bdt = drift * s.dt;
+        s.sig = p->params[1];
+    } else {
+        s.bdt = 0.0;
+        s.sig = 1.0;
+    }
+    return s;
+}
+
+template <int D, int P>
+void launch_step(const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz, cudaStream_t st) {
+    const int warps = 8;
+    const unsigned grid = static_cast<unsigned>((s.cells + warps - 1) / warps);
+    if (zpass)
+        k_srmc_step<D, P, true, false><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+    else if (wantz)
+        k_srmc_step<D, P, false, true><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+    else
+        k_srmc_step<D, P, false, false><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+}
+
+template <int D>
+void launch_step_d(int P, const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz,
+                   cudaStream_t st) {
+    if (P == 1)
+        launch_step<D, 1>(s, next, y, z, zpass, wantz, st);
+    else
+        launch_step<D, D + 1>(s, next, y, z, zpass, wantz, st);
+}
+
+void dispatch_step(int d, int P, const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz,
+                   cudaStream_t st) {
+    switch (d) {
+        case 1: launch_step_d<1>(P, s, next, y, z, zpass, wantz, st); break;
+        case 2: launch_step_d<2>(P, s, next, y, z, zpass, wantz, st); break;
+        case 3: launch_step_d<3>(P, s, next, y, z, zpass, wantz, st); break;
+        case 4: launch_step_d<4>(P, s, next, y, z, zpass, wantz, st); break;
+        case 5: launch_step_d<5>(P, s, next, y, z, zpass, wantz, st); break;
+        default: launch_step_d<6>(P, s, next, y, z, zpass, wantz, st); break;
+    }
+}
+
+template <int D>
+void launch_eval_d(int P, const SrmcDev& s, const double* tab, const double* x, int64_t n, double* out) {
+    const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+    if (P == 1)
+        k_srmc_eval<D, 1><<<grid, 256>>>(s, tab, x, n, out);
+    else
+        k_srmc_eval<D, D + 1><<<grid, 256>>>(s, tab, x, n, out);
+}
+
+#define CK(call)                                                                  \
+    do {                                                                          \
+        cudaError_t e_ = (call);                                                  \
+        if (e_ != cudaSuccess) {                                                  \
+            std::snprintf(msg, sizeof msg, "CUDA: %s (%s)", cudaGetErrorString(e_), #call); \
+            rc = QRMC_ECUDA;                                                      \
+            goto done;                                                            \
+        }                                                                         \
+    } while (0)
+
+}  // namespace
+
+extern "C" int32_t qrmc_srmc_basis_size(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg) {
+    if (validate(prob, cfg, nullptr, 0) != QRMC_OK) return -1;
+    return cfg->basis == QRMC_SRMC_LP1 ? prob->dim + 1 : 1;
+}
+
+extern "C" int64_t qrmc_srmc_cells(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg) {
+    if (validate(prob, cfg, nullptr, 0) != QRMC_OK) return -1;
+    int64_t c = 1;
+    for (int l = 0; l < prob->dim; ++l) c *= cfg->cells_per_dim;
+    return c;
+}
+
+extern "C" int32_t qrmc_srmc_solve(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, double* y,
+                                   size_t y_len, double* z, size_t z_len, qrmc_srmc_stats_t* stats, char* err,
+                                   size_t err_len) {
+    char msg[256] = {0};
+    int rc = validate(prob, cfg, err, err_len);
+    if (rc != QRMC_OK) return rc;
+    const int d = prob->dim;
+    const int P = cfg->basis == QRMC_SRMC_LP1 ? d + 1 : 1;
+    SrmcDev s = make_dev(prob, cfg);
+    const bool zpass = needs_z(prob);
+    const bool wantz = !zpass && cfg->want_z != 0;
+    const size_t per_y = static_cast<size_t>(s.cells) * P;
+    const size_t per_z = per_y * d;
+    const int N = cfg->steps;
+    if (!y || y_len < per_y * N) return set_err(err, err_len, "y buffer too small (steps * cells * P)"), QRMC_EINVAL;
+    const bool outz = z != nullptr;
+    if (outz && z_len < per_z * N) return set_err(err, err_len, "z buffer too small (steps * cells * d * P)"), QRMC_EINVAL;
+    double *dy = nullptr, *dz = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t st = nullptr;
+    const bool anyz = zpass || wantz || outz;
+    float ms = 0.f;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaMalloc(&dy, per_y * N * sizeof(double)));
+    if (anyz) CK(cudaMalloc(&dz, per_z * N * sizeof(double)));
+    CK(cudaEventRecord(e0, st));
+    for (int i = N - 1; i >= 0; --i) {
+        s.step = i;
+        s.last = (i == N - 1);
+        s.t = (i + 1) * s.dt;  // the driver is evaluated at (t_{i+1}, X_{i+1}, Y1, Zhat_i(X_i))
+        dispatch_step(d, P, s, s.last ? nullptr : dy + per_y * (i + 1), dy + per_y * i, anyz ? dz + per_z * i : nullptr,
+                      zpass, !zpass && (wantz || outz), st);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    CK(cudaMemcpyAsync(y, dy, per_y * N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (outz) CK(cudaMemcpyAsync(z, dz, per_z * N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t j = 0; j < per_y; ++j)
+        if (!std::isfinite(y[j])) {
+            std::snprintf(msg, sizeof msg, "non-finite coefficient at step 0");
+            rc = QRMC_ENUMERIC;
+            goto done;
+        }
+    if (stats) {
+        stats->path_steps = static_cast<uint64_t>(s.cells) * static_cast<uint64_t>(s.M) * N * (zpass ? 2u : 1u);
+        stats->device_seconds = ms * 1e-3;
+        stats->kernel_launches = N;
+    }
+done:
+    if (dy) cudaFree(dy);
+    if (dz) cudaFree(dz);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (st) cudaStreamDestroy(st);
+    if (rc != QRMC_OK) set_err(err, err_len, msg);
+    return rc;
+}
+
+extern "C" int32_t qrmc_srmc_evaluate(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg,
+                                      const double* y_step, const double* x, int64_t npts, double* out, char* err,
+                                      size_t err_len) {
+    char msg[256] = {0};
+    int rc = validate(prob, cfg, err, err_len);
+    if (rc != QRMC_OK) return rc;
+    if (npts <= 0) return QRMC_OK;
+    const int d = prob->dim;
+    const int P = cfg->basis == QRMC_SRMC_LP1 ? d + 1 : 1;
+    const SrmcDev s = make_dev(prob, cfg);
+    const size_t tab = static_cast<size_t>(s.cells) * P;
+    double *dt = nullptr, *dx = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&dt, tab * sizeof(double)));
+    CK(cudaMalloc(&dx, npts * d * sizeof(double)));
+    CK(cudaMalloc(&dout, npts * sizeof(double)));
+    CK(cudaMemcpy(dt, y_step, tab * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dx, x, npts * d * sizeof(double), cudaMemcpyHostToDevice));
+    switch (d) {
+        case 1: launch_eval_d<1>(P, s, dt, dx, npts, dout); break;
+        case 2: launch_eval_d<2>(P, s, dt, dx, npts, dout); break;
+        case 3: launch_eval_d<3>(P, s, dt, dx, npts, dout); break;
+        case 4: launch_eval_d<4>(P, s, dt, dx, npts, dout); break;
+        case 5: launch_eval_d<5>(P, s, dt, dx, npts, dout); break;
+        default: launch_eval_d<6>(P, s, dt, dx, npts, dout); break;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dout, npts * sizeof(double), cudaMemcpyDeviceToHost));
+done:
+    if (dt) cudaFree(dt);
+    if (dx) cudaFree(dx);
+    if (dout) cudaFree(dout);
+    if (rc != QRMC_OK) set_err(err, err_len, msg);
+    return rc;
+}

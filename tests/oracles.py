@@ -221,3 +221,46 @@ def ref() -> Oracle:
     if "ref" not in _cache:
         _cache["ref"] = Oracle(REF_PATH, "qrmc_ref_")
     return _cache["ref"]
+
+
+SRMC_PATH = ROOT / "oracle" / "lib" / "libsrmc_oracle.so"
+
+
+class SrmcOracle:
+    """oracle/srmc_oracle.c: CPU restatement of the SRMC scheme (include/qrmc_srmc.h).
+    Parity unpinned against the reference (no SRMC code there); checker only."""
+
+    def __init__(self, path: Path):
+        from paper_2407_21084_b200 import srmc
+        self.srmc = srmc
+        self.L = C.CDLL(str(path))
+        Pp, Cp = C.POINTER(srmc.SrmcProblem), C.POINTER(srmc.SrmcConfig)
+        self.L.srmc_oracle_solve.argtypes = [Pp, Cp, _dp, _dp, C.c_int32]
+        self.L.srmc_oracle_solve.restype = C.c_int32
+        self.L.srmc_oracle_eval.argtypes = [Pp, Cp, _dp, _dp]
+        self.L.srmc_oracle_eval.restype = C.c_double
+
+    def solve(self, prob, cfg, with_z: bool = False, threads: int = 0):
+        d = prob.dim
+        P = d + 1 if cfg.basis == self.srmc.LP1 else 1
+        cells = cfg.cells_per_dim ** d
+        y = np.zeros((cfg.steps, cells, P))
+        z = np.zeros((cfg.steps, cells, d, P)) if with_z else None
+        rc = self.L.srmc_oracle_solve(C.byref(prob), C.byref(cfg), _ptr(y), _ptr(z) if z is not None else None,
+                                      threads)
+        assert rc == 0
+        return y, z
+
+    def evaluate(self, prob, cfg, y_step: np.ndarray, x: np.ndarray) -> np.ndarray:
+        y_step = np.ascontiguousarray(y_step, dtype=np.float64)
+        x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+        return np.array([self.L.srmc_oracle_eval(C.byref(prob), C.byref(cfg), _ptr(y_step), _ptr(row))
+                         for row in x])
+
+
+def srmc_port() -> SrmcOracle:
+    if "srmc" not in _cache:
+        if not SRMC_PATH.exists():
+            raise RuntimeError(f"{SRMC_PATH} missing: run `make -C oracle port`")
+        _cache["srmc"] = SrmcOracle(SRMC_PATH)
+    return _cache["srmc"]

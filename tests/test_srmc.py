@@ -1,0 +1,180 @@
+"""SRMC solver (include/qrmc_srmc.h).
+
+The reference has no SRMC code, so parity is UNPINNED against it. Two checks stand in:
+* replay parity: GPU tables vs the C restatement oracle/srmc_oracle.c on the same Philox
+  draws, |gpu - oracle| <= 1e-9 * max(1, max|oracle|) (FP64; only the reduction order
+  differs), the cell index bit-exact;
+* statistics: the solution against closed forms -- SinBenchmark's exact_solution
+  (proj/src/benchmark.cpp:20-28) and Black-Scholes for the Bergman driver (linear case
+  r_b = r_l; for a call the borrowing branch is always active, so the nonlinear price is
+  Black-Scholes at r_b).
+"""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+import oracles
+from paper_2407_21084_b200 import srmc
+
+TOL = 1e-9
+
+# Bergman test market (Gobet-Lemor-Warin's call: S0 = K = 100, T = 0.5, mu = 5%, sigma = 20%)
+S0, K, T, SIG, MU = 100.0, 100.0, 0.5, 0.2, 0.05
+
+
+def _bergman(d, rl, rb):
+    return srmc.bergman_problem(d, MU, SIG, rl, rb, K, T)
+
+
+def _box(w=1.0):
+    return math.log(S0) - w, math.log(S0) + w
+
+
+# ------------------------------------------------------------------ CPU (no GPU)
+
+def test_library_exports_and_host_validation():
+    L = srmc.lib()
+    for sym in ("qrmc_srmc_basis_size", "qrmc_srmc_cells", "qrmc_srmc_solve", "qrmc_srmc_evaluate"):
+        assert hasattr(L, sym)
+    p = srmc.sin_bench_problem(3)
+    c = srmc.config(4, 5, 64, basis=srmc.LP1)
+    assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(c)) == 4
+    assert L.qrmc_srmc_cells(C.byref(p), C.byref(c)) == 125
+    c0 = srmc.config(4, 5, 64, basis=srmc.LP0)
+    assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(c0)) == 1
+    bad = srmc.config(4, 5, 3, basis=srmc.LP1)  # M < P
+    assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(bad)) == -1
+
+
+@pytest.mark.parametrize("mutate,code", [
+    (lambda p, c: setattr(c, "paths_per_cell", 2), 1),
+    (lambda p, c: setattr(c, "steps", 0), 1),
+    (lambda p, c: setattr(c, "hi", c.lo), 1),
+    (lambda p, c: setattr(c, "truncation", 0.0), 1),
+    (lambda p, c: setattr(p, "kind", 9), 7),
+    (lambda p, c: setattr(p, "dim", 7), 1),
+    (lambda p, c: (setattr(c, "cells_per_dim", 2000), setattr(c, "paths_per_cell", 10**6)), 4),
+])
+def test_solve_rejects_bad_input_before_touching_the_device(mutate, code):
+    p = srmc.sin_bench_problem(2)
+    c = srmc.config(3, 4, 64)
+    mutate(p, c)
+    with pytest.raises(srmc.SrmcError) as e:
+        srmc.solve(p, c)
+    assert e.value.code == code
+
+
+def test_oracle_sin_bench_converges_to_exact_solution():
+    o = oracles.srmc_port()
+    p = srmc.sin_bench_problem(1)
+    c = srmc.config(10, 64, 8000, basis=srmc.LP1, lo=-4.0, hi=4.0)
+    y, _ = o.solve(p, c)
+    x = np.linspace(-2.0, 2.0, 41)[:, None]
+    err = o.evaluate(p, c, y[0], x) - srmc.sin_bench_exact(0.0, x)
+    assert np.abs(err).max() < 0.015, np.abs(err).max()
+
+
+@pytest.mark.parametrize("rb", [0.01, 0.06])
+def test_oracle_bergman_matches_black_scholes(rb):
+    o = oracles.srmc_port()
+    lo, hi = _box()
+    p = _bergman(1, 0.01, rb)
+    c = srmc.config(10, 127, 4000, basis=srmc.LP1, lo=lo, hi=hi)  # odd: x0 sits at a cell centre
+    y, _ = o.solve(p, c)
+    u = o.evaluate(p, c, y[0], np.array([[math.log(S0)]]))[0]
+    bs = srmc.bergman_linear_exact([math.log(S0)], SIG, rb, K, T)
+    assert abs(u - bs) < 0.02 * bs, (u, bs)
+
+
+# ------------------------------------------------------------------ GPU
+
+PARITY_CASES = [
+    ("sin-d1-lp0", lambda: srmc.sin_bench_problem(1), dict(steps=5, cells_per_dim=16, paths_per_cell=45, basis=srmc.LP0)),
+    ("sin-d2-lp1-z", lambda: srmc.sin_bench_problem(2), dict(steps=4, cells_per_dim=8, paths_per_cell=64, basis=srmc.LP1, want_z=True)),
+    ("sin-d3-lp1", lambda: srmc.sin_bench_problem(3), dict(steps=3, cells_per_dim=5, paths_per_cell=37, basis=srmc.LP1)),
+    ("sin-d6-lp1-one-cell", lambda: srmc.sin_bench_problem(6), dict(steps=3, cells_per_dim=1, paths_per_cell=300, basis=srmc.LP1)),
+    ("sin-d4-lp0-trunc", lambda: srmc.sin_bench_problem(4), dict(steps=3, cells_per_dim=4, paths_per_cell=33, basis=srmc.LP0, truncation=1.7)),
+    ("bergman-d1-lp1", lambda: _bergman(1, 0.01, 0.06), dict(steps=5, cells_per_dim=32, paths_per_cell=100, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
+    ("bergman-d2-lp1", lambda: _bergman(2, 0.01, 0.06), dict(steps=4, cells_per_dim=8, paths_per_cell=96, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
+    ("bergman-d3-lp0", lambda: _bergman(3, 0.02, 0.05), dict(steps=3, cells_per_dim=4, paths_per_cell=50, basis=srmc.LP0, lo=_box()[0], hi=_box()[1])),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,mk,kw", PARITY_CASES, ids=[c[0] for c in PARITY_CASES])
+def test_gpu_tables_match_oracle_on_replayed_draws(name, mk, kw):
+    p = mk()
+    c = srmc.config(seed=7, **kw)
+    want_z = bool(kw.get("want_z")) or p.kind == srmc.BERGMAN
+    got = srmc.solve(p, c, with_z=want_z)
+    y, z = oracles.srmc_port().solve(p, c, with_z=want_z)
+    scale = max(1.0, float(np.abs(y).max()))
+    assert np.abs(got.y - y).max() <= TOL * scale
+    if want_z:
+        zs = max(1.0, float(np.abs(z).max()))
+        assert np.abs(got.z - z).max() <= TOL * zs
+    cells = c.cells_per_dim ** p.dim
+    assert got.stats["path_steps"] == cells * c.paths_per_cell * c.steps * (2 if p.kind == srmc.BERGMAN else 1)
+    assert got.stats["kernel_launches"] == c.steps
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,n", [(1, 7), (2, 16), (3, 9), (6, 4)])
+def test_gpu_cell_index_bit_exact(d, n):
+    """LP0 table holding its own cell number: evaluate() must return exactly the oracle's
+    cell, for points inside, on cell faces and outside the box (projection)."""
+    p = srmc.sin_bench_problem(d)
+    c = srmc.config(1, n, 8, basis=srmc.LP0, lo=-1.3, hi=2.9)
+    cells = n ** d
+    tab = np.arange(cells, dtype=np.float64)[:, None]
+    rng = np.random.default_rng(d * 100 + n)
+    h = (c.hi - c.lo) / n
+    x = np.concatenate([
+        rng.uniform(c.lo - 1.0, c.hi + 1.0, (3000, d)),
+        c.lo + h * rng.integers(0, n + 1, (1000, d)).astype(np.float64),  # exactly on faces
+        np.full((1, d), c.lo), np.full((1, d), c.hi),
+    ])
+    tables = srmc.SrmcTables(p, c, tab[None], None)
+    got = tables.evaluate(0, x)
+    want = oracles.srmc_port().evaluate(p, c, tab, x)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_gpu_evaluate_matches_oracle_lp1():
+    p = srmc.sin_bench_problem(3)
+    c = srmc.config(3, 6, 64, basis=srmc.LP1)
+    t = srmc.solve(p, c)
+    x = np.random.default_rng(3).uniform(-5, 5, (500, 3))
+    want = oracles.srmc_port().evaluate(p, c, t.y[0], x)
+    assert np.abs(t.evaluate(0, x) - want).max() <= 1e-13
+
+
+@pytest.mark.gpu
+def test_gpu_sin_bench_d4_lp1_agrees_with_exact_solution():
+    p = srmc.sin_bench_problem(4)
+    c = srmc.config(10, 16, 1000, basis=srmc.LP1, lo=-4.0, hi=4.0)
+    t = srmc.solve(p, c)
+    x = np.random.default_rng(1).uniform(-1.5, 1.5, (400, 4))
+    err = t.evaluate(0, x) - srmc.sin_bench_exact(0.0, x)
+    assert np.abs(err).mean() < 0.01, np.abs(err).mean()
+    assert np.abs(err).max() < 0.05, np.abs(err).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rb", [0.01, 0.06])
+def test_gpu_bergman_d4_agrees_with_black_scholes(rb):
+    lo, hi = _box(0.6)
+    p = _bergman(4, 0.01, rb)
+    # odd cell count: x0 sits at a cell centre, where the LP1 fit is its (lowest-variance)
+    # constant term; at a cell face the slope noise enters with weight 1
+    c = srmc.config(10, 15, 4000, basis=srmc.LP1, lo=lo, hi=hi)
+    t = srmc.solve(p, c, with_z=True)
+    x0 = np.full((1, 4), math.log(S0))
+    u = t.evaluate(0, x0)[0]
+    bs = srmc.bergman_linear_exact(x0[0], SIG, rb, K, T)
+    assert abs(u - bs) < 0.03 * bs, (u, bs)
+    if rb > 0.01:  # the borrowing premium is visible
+        assert u > srmc.bergman_linear_exact(x0[0], SIG, 0.01, K, T) + 0.5 * (bs - srmc.bergman_linear_exact(x0[0], SIG, 0.01, K, T))
