@@ -83,6 +83,15 @@ int32_t qrmc_srmc_evaluate(const qrmc_srmc_problem_t* prob, const qrmc_srmc_conf
                            const double* y_step, const double* x, int64_t npts, double* out,
                            char* err, size_t err_len);
 
+/* One backward step on DEVICE tables for the cells [k_begin, k_end) on `stream`
+ * (cudaStream_t, NULL = legacy default): next_dev = step-(step+1) y table (unused at the
+ * last step), y_dev / z_dev = step-`step` tables (full size; only the range is written;
+ * z_dev may be NULL when the driver does not read z). Enqueue only (no sync). The sharded
+ * driver (srmc.py solve_sharded) calls it per rank and all-gathers each step's table. */
+int32_t qrmc_srmc_step_device(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, int32_t step,
+                              const double* next_dev, double* y_dev, double* z_dev, int64_t k_begin,
+                              int64_t k_end, void* stream, char* err, size_t err_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -171,48 +171,62 @@ static void s_cell(const srmc_t* s, int step, const double* next, int64_t k, int
         for (int j = 0; j < d * P; ++j) zout[j] = bz[j];
 }
 
+static void s_init(srmc_t* s, const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg) {
+    memset(s, 0, sizeof *s);
+    s->kind = prob->kind;
+    s->d = prob->dim;
+    s->n = cfg->cells_per_dim;
+    s->P = cfg->basis == QRMC_SRMC_LP1 ? s->d + 1 : 1;
+    s->cells = 1;
+    for (int l = 0; l < s->d; ++l) s->cells *= s->n;
+    s->M = cfg->paths_per_cell;
+    s->seed = cfg->seed;
+    s->lo = cfg->lo;
+    s->hi = cfg->hi;
+    s->h = (cfg->hi - cfg->lo) / cfg->cells_per_dim;
+    s->inv2h = 2.0 / s->h;
+    s->T = prob->horizon;
+    s->dt = prob->horizon / cfg->steps;
+    s->sqrt_dt = sqrt(s->dt);
+    s->L = cfg->truncation;
+    for (int j = 0; j < 8; ++j) s->p[j] = prob->params[j];
+    if (s->kind == QRMC_SRMC_BERGMAN) {
+        const double drift = prob->params[0] - 0.5 * (prob->params[1] * prob->params[1]);
+        s->bdt = drift * s->dt;
+        s->sig = prob->params[1];
+    } else {
+        s->bdt = 0.0;
+        s->sig = 1.0;
+    }
+}
+
+/* one backward step over the cells [k_begin, k_end) (a rank's shard in the sharded tests);
+ * y_step / z_step are the full step tables, next = step+1's y table */
+int32_t srmc_oracle_step(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, int32_t step,
+                         const double* next, double* y_step, double* z_step, int64_t k_begin, int64_t k_end,
+                         int32_t threads) {
+    srmc_t s;
+    s_init(&s, prob, cfg);
+    s.last = (step == cfg->steps - 1);
+    s.t = (step + 1) * s.dt; /* f at (t_{i+1}, X_{i+1}, Y1, Zhat_i(X_i)) */
+    const int zpass = prob->kind == QRMC_SRMC_BERGMAN;
+    const int anyz = zpass || cfg->want_z || z_step != NULL;
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t k = k_begin; k < k_end; ++k)
+        s_cell(&s, step, s.last ? NULL : next, k, zpass, anyz, y_step + k * s.P,
+               z_step ? z_step + k * s.d * s.P : NULL);
+    return 0;
+}
+
 int32_t srmc_oracle_solve(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, double* y, double* z,
                           int32_t threads) {
     srmc_t s;
-    memset(&s, 0, sizeof s);
-    s.kind = prob->kind;
-    s.d = prob->dim;
-    s.n = cfg->cells_per_dim;
-    s.P = cfg->basis == QRMC_SRMC_LP1 ? s.d + 1 : 1;
-    s.cells = 1;
-    for (int l = 0; l < s.d; ++l) s.cells *= s.n;
-    s.M = cfg->paths_per_cell;
-    s.seed = cfg->seed;
-    s.lo = cfg->lo;
-    s.hi = cfg->hi;
-    s.h = (cfg->hi - cfg->lo) / cfg->cells_per_dim;
-    s.inv2h = 2.0 / s.h;
-    s.T = prob->horizon;
-    s.dt = prob->horizon / cfg->steps;
-    s.sqrt_dt = sqrt(s.dt);
-    s.L = cfg->truncation;
-    for (int j = 0; j < 8; ++j) s.p[j] = prob->params[j];
-    if (s.kind == QRMC_SRMC_BERGMAN) {
-        const double drift = prob->params[0] - 0.5 * (prob->params[1] * prob->params[1]);
-        s.bdt = drift * s.dt;
-        s.sig = prob->params[1];
-    } else {
-        s.bdt = 0.0;
-        s.sig = 1.0;
-    }
-    const int zpass = prob->kind == QRMC_SRMC_BERGMAN;
-    const int anyz = zpass || cfg->want_z || z != NULL;
+    s_init(&s, prob, cfg);
     const size_t per_y = (size_t)s.cells * s.P, per_z = per_y * s.d;
-    if (threads > 0) omp_set_num_threads(threads);
-    for (int i = cfg->steps - 1; i >= 0; --i) {
-        srmc_t si = s;
-        si.last = (i == cfg->steps - 1);
-        si.t = (i + 1) * s.dt; /* f at (t_{i+1}, X_{i+1}, Y1, Zhat_i(X_i)) */
-        const double* next = si.last ? NULL : y + per_y * (i + 1);
-#pragma omp parallel for schedule(dynamic, 16)
-        for (int64_t k = 0; k < s.cells; ++k)
-            s_cell(&si, i, next, k, zpass, anyz, y + per_y * i + k * s.P, z ? z + per_z * i + k * s.d * s.P : NULL);
-    }
+    for (int i = cfg->steps - 1; i >= 0; --i)
+        srmc_oracle_step(prob, cfg, i, i == cfg->steps - 1 ? NULL : y + per_y * (i + 1), y + per_y * i,
+                         z ? z + per_z * i : NULL, 0, s.cells, threads);
     return 0;
 }
 

@@ -34,10 +34,12 @@ using namespace qrmc_dev;
 struct SrmcDev {
     int kind, n, step, last;
     int64_t cells, M;
+    int64_t k0, k1;  // this launch's cell range [k0, k1) (a rank's shard; [0, cells) single-GPU)
     uint64_t seed;
     double lo, hi, h, inv2h, dt, sqrt_dt, t, T, L;
     double p[8];
     double bdt, sig;  // Euler: x + bdt + sig * sqrt_dt * z
+    double decay;     // SinBenchmark exp(lambda^2 d (t - T) / 2) at this step's t (hoisted per launch)
 };
 
 template <int D>
@@ -57,9 +59,7 @@ __device__ __forceinline__ double srmc_driver(const SrmcDev& s, const double* x,
         double sum = 0.0;
 #pragma unroll
         for (int l = 0; l < D; ++l) sum = DADD(sum, x[l]);
-        const double lam = s.p[1];
-        const double e = exp(DDIV(DMUL(DMUL(DMUL(lam, lam), static_cast<double>(D)), DSUB(s.t, s.T)), 2.0));
-        const double w = DSUB(DSUB(DSUB(y, s.p[0]), 1.0), DMUL(sin(DMUL(lam, sum)), e));
+        const double w = DSUB(DSUB(DSUB(y, s.p[0]), 1.0), DMUL(sin(DMUL(s.p[1], sum)), s.decay));
         const double ww = DMUL(w, w);
         return ww < 1.0 ? ww : 1.0;
     }
@@ -203,13 +203,13 @@ __device__ __forceinline__ void acc_gram(double* A, const double* phi) {
 // ZPASS: the driver reads z -> pass 1 fits Z, pass 2 replays and fits Y.
 // WANTZ: fit Z alongside Y in a single pass (driver without z).
 template <int D, int P, bool ZPASS, bool WANTZ>
-__global__ void __launch_bounds__(256) k_srmc_step(SrmcDev s, const double* __restrict__ next,
+__global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P >= 20 ? 1 : 2))) k_srmc_step(SrmcDev s, const double* __restrict__ next,
                                                    double* __restrict__ ytab, double* __restrict__ ztab) {
     constexpr int NA = P * (P + 1) / 2;
     constexpr bool ANYZ = ZPASS || WANTZ;
     const int lane = threadIdx.x & 31;
-    const int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (k >= s.cells) return;  // whole warps exit together
+    const int64_t k = s.k0 + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (k >= s.k1) return;  // whole warps exit together
     int cc[D];
     {
         int64_t r = k;
@@ -330,6 +330,8 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
     s.cells = 1;
     for (int l = 0; l < p->dim; ++l) s.cells *= c->cells_per_dim;
     s.M = c->paths_per_cell;
+    s.k0 = 0;
+    s.k1 = s.cells;
     s.seed = c->seed;
     s.lo = c->lo;
     s.hi = c->hi;
@@ -354,7 +356,8 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
 template <int D, int P>
 void launch_step(const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz, cudaStream_t st) {
     const int warps = 8;
-    const unsigned grid = static_cast<unsigned>((s.cells + warps - 1) / warps);
+    const unsigned grid = static_cast<unsigned>((s.k1 - s.k0 + warps - 1) / warps);
+    if (grid == 0) return;
     if (zpass)
         k_srmc_step<D, P, true, false><<<grid, warps * 32, 0, st>>>(s, next, y, z);
     else if (wantz)
@@ -449,6 +452,7 @@ extern "C" int32_t qrmc_srmc_solve(const qrmc_srmc_problem_t* prob, const qrmc_s
         s.step = i;
         s.last = (i == N - 1);
         s.t = (i + 1) * s.dt;  // the driver is evaluated at (t_{i+1}, X_{i+1}, Y1, Zhat_i(X_i))
+        s.decay = std::exp(((s.p[1] * s.p[1]) * static_cast<double>(d)) * (s.t - s.T) / 2.0);
         dispatch_step(d, P, s, s.last ? nullptr : dy + per_y * (i + 1), dy + per_y * i, anyz ? dz + per_z * i : nullptr,
                       zpass, !zpass && (wantz || outz), st);
         CK(cudaGetLastError());
@@ -511,6 +515,38 @@ done:
     if (dt) cudaFree(dt);
     if (dx) cudaFree(dx);
     if (dout) cudaFree(dout);
+    if (rc != QRMC_OK) set_err(err, err_len, msg);
+    return rc;
+}
+
+// One backward step on caller-owned device tables for the cell range [k_begin, k_end):
+// the sharded (multi-GPU) driver runs it on its own cells, then all-gathers the step's
+// table (paper_2407_21084_b200/srmc.py, solve_sharded). Results per cell do not depend
+// on the range, so a sharded solve is bitwise identical to the single-GPU one.
+extern "C" int32_t qrmc_srmc_step_device(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, int32_t step,
+                                         const double* next_dev, double* y_dev, double* z_dev, int64_t k_begin,
+                                         int64_t k_end, void* stream, char* err, size_t err_len) {
+    char msg[256] = {0};
+    int rc = validate(prob, cfg, err, err_len);
+    if (rc != QRMC_OK) return rc;
+    SrmcDev s = make_dev(prob, cfg);
+    if (step < 0 || step >= cfg->steps) return set_err(err, err_len, "step out of range"), QRMC_EINVAL;
+    if (k_begin < 0 || k_end < k_begin || k_end > s.cells) return set_err(err, err_len, "bad cell range"), QRMC_EINVAL;
+    const bool zpass = needs_z(prob);
+    if (!y_dev || (step < cfg->steps - 1 && !next_dev) || (zpass && !z_dev))
+        return set_err(err, err_len, "null device table"), QRMC_EINVAL;
+    const int d = prob->dim;
+    const int P = cfg->basis == QRMC_SRMC_LP1 ? d + 1 : 1;
+    s.k0 = k_begin;
+    s.k1 = k_end;
+    s.step = step;
+    s.last = (step == cfg->steps - 1);
+    s.t = (step + 1) * s.dt;
+    s.decay = std::exp(((s.p[1] * s.p[1]) * static_cast<double>(d)) * (s.t - s.T) / 2.0);
+    dispatch_step(d, P, s, s.last ? nullptr : next_dev, y_dev, z_dev, zpass, !zpass && z_dev != nullptr,
+                  static_cast<cudaStream_t>(stream));
+    CK(cudaGetLastError());
+done:
     if (rc != QRMC_OK) set_err(err, err_len, msg);
     return rc;
 }

@@ -156,3 +156,71 @@ def solve(problem: SrmcProblem, cfg: SrmcConfig, with_z: bool = False) -> SrmcTa
         raise SrmcError(rc, err.value.decode())
     return SrmcTables(problem, cfg, y, z, {"path_steps": st.path_steps, "device_seconds": st.device_seconds,
                                           "kernel_launches": st.kernel_launches})
+
+
+def _device_step_fn(problem: SrmcProblem, cfg: SrmcConfig):
+    """step_fn for solve_sharded: qrmc_srmc_step_device on the current CUDA stream."""
+    import torch
+    L = lib()
+    L.qrmc_srmc_step_device.argtypes = [C.POINTER(SrmcProblem), C.POINTER(SrmcConfig), C.c_int32, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_char_p,
+                                        C.c_size_t]
+    L.qrmc_srmc_step_device.restype = C.c_int32
+    err = C.create_string_buffer(256)
+
+    def step(i, nxt, y, z, k0, k1):
+        rc = L.qrmc_srmc_step_device(C.byref(problem), C.byref(cfg), i, nxt.data_ptr() if nxt is not None else None,
+                                     y.data_ptr(), z.data_ptr() if z is not None else None, k0, k1,
+                                     torch.cuda.current_stream().cuda_stream, err, 256)
+        if rc:
+            raise SrmcError(rc, err.value.decode())
+    return step
+
+
+def solve_sharded(problem: SrmcProblem, cfg: SrmcConfig, with_z: bool = False, group=None, step_fn=None,
+                  device=None) -> SrmcTables:
+    """SRMC backward solve with the hypercubes partitioned over the ranks of ``group``
+    (north_star item 5): rank r owns cells [r*c, min((r+1)*c, cells)), c = ceil(cells / G),
+    runs each backward step on its cells only, and the step's y table is all-gathered
+    (NCCL over NVLink on GPUs) before the next step, because paths land in arbitrary cells.
+    Z is only read inside its own cell, so it is gathered once at the end (when asked for).
+    Every cell's coefficients depend on nothing but (seed, step, cell) and the gathered
+    table, so the result is bitwise identical for every G. ``step_fn(i, next, y, z, k0, k1)``
+    defaults to the CUDA kernel; the CPU tests inject the oracle's per-range step."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    d = problem.dim
+    P = d + 1 if cfg.basis == LP1 else 1
+    cells = cfg.cells_per_dim ** d
+    per = -(-cells // world)
+    rows = per * world
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device()) if step_fn is None else torch.device("cpu")
+    step_fn = step_fn or _device_step_fn(problem, cfg)
+    N = cfg.steps
+    needz = with_z or problem.kind == BERGMAN
+    y = torch.zeros((N, rows, P), dtype=torch.float64, device=device)
+    z = torch.zeros((N, rows, d, P), dtype=torch.float64, device=device) if needz else None
+    k0, k1 = min(rank * per, cells), min((rank + 1) * per, cells)
+
+    def gather(full: torch.Tensor) -> None:
+        if world == 1:
+            return
+        mine = full[rank * per:(rank + 1) * per].clone()
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(full, mine, group=group)
+        else:
+            dist.all_gather(list(full.chunk(world)), mine, group=group)
+
+    for i in range(N - 1, -1, -1):
+        step_fn(i, y[i + 1] if i + 1 < N else None, y[i], z[i] if needz else None, k0, k1)
+        gather(y[i])
+    if with_z and world > 1:
+        for i in range(N):
+            gather(z[i])
+    yh = y[:, :cells].cpu().numpy()
+    zh = z[:, :cells].cpu().numpy() if with_z else None
+    return SrmcTables(problem, cfg, yh, zh, {"path_steps": (k1 - k0) * cfg.paths_per_cell * N *
+                                             (2 if problem.kind == BERGMAN else 1), "cells": (k0, k1)})

@@ -264,3 +264,16 @@ def srmc_port() -> SrmcOracle:
             raise RuntimeError(f"{SRMC_PATH} missing: run `make -C oracle port`")
         _cache["srmc"] = SrmcOracle(SRMC_PATH)
     return _cache["srmc"]
+
+
+def srmc_oracle_step_fn(prob, cfg, threads: int = 1):
+    """step_fn for srmc.solve_sharded on CPU tensors: the oracle's per-range step."""
+    o = srmc_port()
+    Pp, Cp = C.POINTER(o.srmc.SrmcProblem), C.POINTER(o.srmc.SrmcConfig)
+    o.L.srmc_oracle_step.argtypes = [Pp, Cp, C.c_int32, _dp, _dp, _dp, C.c_int64, C.c_int64, C.c_int32]
+    o.L.srmc_oracle_step.restype = C.c_int32
+
+    def step(i, nxt, y, z, k0, k1):
+        p = lambda t: C.cast(t.data_ptr(), _dp) if t is not None else None  # noqa: E731
+        assert o.L.srmc_oracle_step(C.byref(prob), C.byref(cfg), i, p(nxt), p(y), p(z), k0, k1, threads) == 0
+    return step

@@ -178,3 +178,29 @@ def test_gpu_bergman_d4_agrees_with_black_scholes(rb):
     assert abs(u - bs) < 0.03 * bs, (u, bs)
     if rb > 0.01:  # the borrowing premium is visible
         assert u > srmc.bergman_linear_exact(x0[0], SIG, 0.01, K, T) + 0.5 * (bs - srmc.bergman_linear_exact(x0[0], SIG, 0.01, K, T))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,mk,kw", [PARITY_CASES[1], PARITY_CASES[6]], ids=[PARITY_CASES[1][0], PARITY_CASES[6][0]])
+def test_gpu_per_range_steps_are_bitwise_equal_to_the_whole_solve(name, mk, kw):
+    """qrmc_srmc_step_device over 3 uneven cell ranges per step (what 3 ranks of
+    solve_sharded compute before their all-gather) == qrmc_srmc_solve, bit for bit; and
+    solve_sharded at G=1 (no process group) == qrmc_srmc_solve."""
+    import torch
+    p = mk()
+    c = srmc.config(seed=7, **kw)
+    whole = srmc.solve(p, c, with_z=True)
+    cells, d = c.cells_per_dim ** p.dim, p.dim
+    P = whole.y.shape[2]
+    y = torch.zeros((c.steps, cells, P), dtype=torch.float64, device="cuda")
+    z = torch.zeros((c.steps, cells, d, P), dtype=torch.float64, device="cuda")
+    step = srmc._device_step_fn(p, c)
+    cuts = [0, cells // 5, cells // 5 + 1, cells]
+    for i in range(c.steps - 1, -1, -1):
+        for k0, k1 in zip(cuts[:-1], cuts[1:]):
+            step(i, y[i + 1] if i + 1 < c.steps else None, y[i], z[i], k0, k1)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), whole.y)
+    assert np.array_equal(z.cpu().numpy(), whole.z)
+    g1 = srmc.solve_sharded(p, c, with_z=True)
+    assert np.array_equal(g1.y, whole.y) and np.array_equal(g1.z, whole.z)
