@@ -39,6 +39,7 @@ struct SrmcDev {
     double lo, hi, h, inv2h, dt, sqrt_dt, t, T, L;
     double p[8];
     double bdt, sig;  // Euler: x + bdt + sig * sqrt_dt * z
+    uint32_t rk[20];  // Philox round keys (seed + r * Weyl), read from the constant bank
     double decay;     // SinBenchmark exp(lambda^2 d (t - T) / 2) at this step's t (hoisted per launch)
 };
 
@@ -164,16 +165,33 @@ __device__ __forceinline__ void chol_solve(const double* A, double* b) {
 template <int D, int P>
 __device__ __forceinline__ void srmc_path(const SrmcDev& s, const double* __restrict__ next, const int* cc,
                                           int64_t k, int64_t m, double* x0, double* sl, double* dw, double* x1, double& y1) {
-    Stream rng(s.seed, sid_training(s.step, static_cast<uint64_t>(k) * static_cast<uint64_t>(s.M) + m));
+    // The path's 2D draws are blocks 0..D-1 of its stream (draw n = half n&1 of block n>>1,
+    // rng.hpp:26-65): uniforms 0..D-1 place the start, D..2D-1 are the Gaussian increments.
+    // Round keys come precomputed from the launch parameters (no per-thread key schedule).
+    const uint64_t sid = sid_training(s.step, static_cast<uint64_t>(k) * static_cast<uint64_t>(s.M) + m);
+    uint64_t w[2 * D];
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+        uint4 c = make_uint4(static_cast<uint32_t>(b), 0u, static_cast<uint32_t>(sid), static_cast<uint32_t>(sid >> 32));
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+            const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+            c = make_uint4(hi1 ^ c.y ^ s.rk[2 * r], lo1, hi0 ^ c.w ^ s.rk[2 * r + 1], lo0);
+        }
+        w[2 * b] = (static_cast<uint64_t>(c.y) << 32) | c.x;
+        w[2 * b + 1] = (static_cast<uint64_t>(c.w) << 32) | c.z;
+    }
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double u = rng.next_uniform();
+        const double u = DMUL(DADD(static_cast<double>(w[l] >> 12), 0.5), 0x1p-52);
         x0[l] = DADD(s.lo, DMUL(DADD(static_cast<double>(cc[l]), u), s.h));
         sl[l] = DSUB(DMUL(2.0, u), 1.0);
     }
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        dw[l] = DMUL(s.sqrt_dt, rng.next_normal());
+        const double u = DMUL(DADD(static_cast<double>(w[D + l] >> 12), 0.5), 0x1p-52);
+        dw[l] = DMUL(s.sqrt_dt, qrmc_normal_quantile(u));
         x1[l] = DADD(DADD(x0[l], s.bdt), DMUL(s.sig, dw[l]));
     }
     if (s.last) {
@@ -333,6 +351,10 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
     s.k0 = 0;
     s.k1 = s.cells;
     s.seed = c->seed;
+    for (int r = 0; r < 10; ++r) {  // Philox4x32-10 key schedule (rng.cpp:9-40)
+        s.rk[2 * r] = static_cast<uint32_t>(c->seed) + static_cast<uint32_t>(r) * 0x9E3779B9u;
+        s.rk[2 * r + 1] = static_cast<uint32_t>(c->seed >> 32) + static_cast<uint32_t>(r) * 0xBB67AE85u;
+    }
     s.lo = c->lo;
     s.hi = c->hi;
     s.h = (c->hi - c->lo) / c->cells_per_dim;
