@@ -35,9 +35,16 @@ def _box(w=1.0):
 # ------------------------------------------------------------------ CPU (no GPU)
 
 def test_library_exports_and_host_validation():
+    import re
+    from pathlib import Path
     L = srmc.lib()
-    for sym in ("qrmc_srmc_basis_size", "qrmc_srmc_cells", "qrmc_srmc_solve", "qrmc_srmc_evaluate"):
-        assert hasattr(L, sym)
+    text = (Path(__file__).resolve().parents[1] / "include" / "qrmc_srmc.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    declared = set(re.findall(r"\b(qrmc_srmc_\w+)\s*\(", text))
+    assert declared == {"qrmc_srmc_basis_size", "qrmc_srmc_cells", "qrmc_srmc_solve", "qrmc_srmc_evaluate",
+                        "qrmc_srmc_step_device"}
+    for sym in declared:
+        assert hasattr(L, sym), sym
     p = srmc.sin_bench_problem(3)
     c = srmc.config(4, 5, 64, basis=srmc.LP1)
     assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(c)) == 4
@@ -46,6 +53,14 @@ def test_library_exports_and_host_validation():
     assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(c0)) == 1
     bad = srmc.config(4, 5, 3, basis=srmc.LP1)  # M < P
     assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(bad)) == -1
+
+
+def test_srmc_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", str(srmc.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
 
 
 @pytest.mark.parametrize("mutate,code", [
