@@ -42,8 +42,18 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="one short workload (for ncu)")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--sweep", action="store_true", help="BASELINE config 5: M x N sweep (1 GPU)")
     a = ap.parse_args()
-    for name, (mk, kw) in (QUICK if a.quick else WORKLOADS).items():
+    todo = QUICK if a.quick else WORKLOADS
+    if a.sweep:
+        todo = {}
+        for M in (100, 1000, 10000):
+            for N in (10, 20, 50, 100):
+                todo[f"c5-sin-d2-lp1-64^2-N{N}-M{M}"] = (lambda: srmc.sin_bench_problem(2),
+                                                        dict(steps=N, cells_per_dim=64, paths_per_cell=M))
+                todo[f"c5-sin-d6-lp0-8^6-N{N}-M{M}"] = (lambda: srmc.sin_bench_problem(6),
+                                                       dict(steps=N, cells_per_dim=8, paths_per_cell=M, basis=srmc.LP0))
+    for name, (mk, kw) in todo.items():
         p, c = mk(), srmc.config(**kw)
         srmc.solve(p, c)  # warm-up (module load, allocations)
         best_dev, best_e2e, st = math.inf, math.inf, None
