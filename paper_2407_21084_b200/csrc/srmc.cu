@@ -97,12 +97,13 @@ __device__ __forceinline__ double srmc_eval(const SrmcDev& s, const double* __re
     return v;
 }
 
-template <int NV>
+// butterfly over the G lanes of one hypercube (xor offsets < G stay inside the group)
+template <int NV, int G>
 __device__ __forceinline__ void warp_sum(double* a) {
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a[j] += __shfl_xor_sync(0xffffffffu, a[j], o);
+        for (int o = G / 2; o > 0; o >>= 1) a[j] += __shfl_xor_sync(0xffffffffu, a[j], o);
     }
 }
 
@@ -220,14 +221,21 @@ __device__ __forceinline__ void acc_gram(double* A, const double* phi) {
 
 // ZPASS: the driver reads z -> pass 1 fits Z, pass 2 replays and fits Y.
 // WANTZ: fit Z alongside Y in a single pass (driver without z).
-template <int D, int P, bool ZPASS, bool WANTZ>
+// G lanes per hypercube: 32 (one warp) normally, 8 when M is small so the per-cell
+// butterfly + Cholesky is amortised over more path iterations per lane.
+template <int D, int P, bool ZPASS, bool WANTZ, int G>
 __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P >= 20 ? 1 : 2))) k_srmc_step(SrmcDev s, const double* __restrict__ next,
                                                    double* __restrict__ ytab, double* __restrict__ ztab) {
     constexpr int NA = P * (P + 1) / 2;
     constexpr bool ANYZ = ZPASS || WANTZ;
     const int lane = threadIdx.x & 31;
-    const int64_t k = s.k0 + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (k >= s.k1) return;  // whole warps exit together
+    const int sub = lane & (G - 1);
+    const int64_t kfirst =
+        s.k0 + (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G);
+    if (kfirst >= s.k1) return;  // whole warps exit together
+    const int64_t k = kfirst + lane / G;
+    const bool live = k < s.k1;  // a tail group past the range still joins the shuffles
+    const int64_t mend = live ? s.M : 0;
     int cc[D];
     {
         int64_t r = k;
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
 
     double x0[D], sl[D], dw[D], x1[D], phi[P], y1;
     const double zero_z[D] = {};
-    for (int64_t m = lane; m < s.M; m += 32) {
+    for (int64_t m = sub; m < mend; m += G) {
         srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1);
         phi_of<D, P>(sl, phi);
         acc_gram<D, P>(A, phi);
@@ -267,13 +275,13 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
             for (int p = 0; p < P; ++p) by[p] += ry * phi[p];
         }
     }
-    warp_sum<NA>(A);
+    warp_sum<NA, G>(A);
     if constexpr (ANYZ) {
-        warp_sum<D * P>(bz);
+        warp_sum<D * P, G>(bz);
         chol_solve<P, D>(A, bz);
     }
     if constexpr (ZPASS) {
-        for (int64_t m = lane; m < s.M; m += 32) {
+        for (int64_t m = sub; m < mend; m += G) {
             srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1);
             phi_of<D, P>(sl, phi);
             double zi[D];
@@ -289,9 +297,9 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
             for (int p = 0; p < P; ++p) by[p] += ry * phi[p];
         }
     }
-    warp_sum<P>(by);
+    warp_sum<P, G>(by);
     chol_solve<P, 1>(A, by);
-    if (lane == 0) {
+    if (live && sub == 0) {
 #pragma unroll
         for (int p = 0; p < P; ++p) ytab[k * P + p] = by[p];
         if constexpr (ANYZ) {
@@ -378,14 +386,28 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
 template <int D, int P>
 void launch_step(const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz, cudaStream_t st) {
     const int warps = 8;
-    const unsigned grid = static_cast<unsigned>((s.k1 - s.k0 + warps - 1) / warps);
+    const int64_t cells = s.k1 - s.k0;
+    // 8 lanes per hypercube, 4 hypercubes per warp -- only when the range still fills the
+    // GPU with quarter as many warps (64^2 cells at M=100: 1.33e10 -> 1.1e10 otherwise)
+    if (s.M < 256 && s.cells >= 32768) {  // by the TOTAL cell count: a shard computes exactly what the whole solve does
+        const unsigned grid = static_cast<unsigned>((cells + warps * 4 - 1) / (warps * 4));
+        if (grid == 0) return;
+        if (zpass)
+            k_srmc_step<D, P, true, false, 8><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+        else if (wantz)
+            k_srmc_step<D, P, false, true, 8><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+        else
+            k_srmc_step<D, P, false, false, 8><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+        return;
+    }
+    const unsigned grid = static_cast<unsigned>((cells + warps - 1) / warps);
     if (grid == 0) return;
     if (zpass)
-        k_srmc_step<D, P, true, false><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+        k_srmc_step<D, P, true, false, 32><<<grid, warps * 32, 0, st>>>(s, next, y, z);
     else if (wantz)
-        k_srmc_step<D, P, false, true><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+        k_srmc_step<D, P, false, true, 32><<<grid, warps * 32, 0, st>>>(s, next, y, z);
     else
-        k_srmc_step<D, P, false, false><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+        k_srmc_step<D, P, false, false, 32><<<grid, warps * 32, 0, st>>>(s, next, y, z);
 }
 
 template <int D>

@@ -109,6 +109,9 @@ PARITY_CASES = [
     ("sin-d1-lp0", lambda: srmc.sin_bench_problem(1), dict(steps=5, cells_per_dim=16, paths_per_cell=45, basis=srmc.LP0)),
     ("sin-d2-lp1-z", lambda: srmc.sin_bench_problem(2), dict(steps=4, cells_per_dim=8, paths_per_cell=64, basis=srmc.LP1, want_z=True)),
     ("sin-d3-lp1", lambda: srmc.sin_bench_problem(3), dict(steps=3, cells_per_dim=5, paths_per_cell=37, basis=srmc.LP1)),
+    # >= 32768 cells and M < 256: 8 lanes per hypercube (4 per warp), 33^3 leaves a tail group
+    ("sin-d3-lp1-subwarp", lambda: srmc.sin_bench_problem(3), dict(steps=2, cells_per_dim=33, paths_per_cell=40, basis=srmc.LP1, want_z=True)),
+    ("bergman-d3-lp1-subwarp", lambda: _bergman(3, 0.01, 0.06), dict(steps=2, cells_per_dim=33, paths_per_cell=24, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
     ("sin-d6-lp1-one-cell", lambda: srmc.sin_bench_problem(6), dict(steps=3, cells_per_dim=1, paths_per_cell=300, basis=srmc.LP1)),
     ("sin-d4-lp0-trunc", lambda: srmc.sin_bench_problem(4), dict(steps=3, cells_per_dim=4, paths_per_cell=33, basis=srmc.LP0, truncation=1.7)),
     ("bergman-d1-lp1", lambda: _bergman(1, 0.01, 0.06), dict(steps=5, cells_per_dim=32, paths_per_cell=100, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
@@ -196,7 +199,7 @@ def test_gpu_bergman_d4_agrees_with_black_scholes(rb):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,mk,kw", [PARITY_CASES[1], PARITY_CASES[6]], ids=[PARITY_CASES[1][0], PARITY_CASES[6][0]])
+@pytest.mark.parametrize("name,mk,kw", [PARITY_CASES[i] for i in (1, 3, 8)], ids=[PARITY_CASES[i][0] for i in (1, 3, 8)])
 def test_gpu_per_range_steps_are_bitwise_equal_to_the_whole_solve(name, mk, kw):
     """qrmc_srmc_step_device over 3 uneven cell ranges per step (what 3 ranks of
     solve_sharded compute before their all-gather) == qrmc_srmc_solve, bit for bit; and
