@@ -162,6 +162,10 @@ __device__ __forceinline__ void chol_solve(const double* A, double* b) {
     }
 }
 
+// The quantile is called 2-pass x D times per path; one out-of-line copy keeps the
+// kernel's instruction footprint small (bit-identical arithmetic).
+__device__ __noinline__ double srmc_normal_quantile(double u) { return qrmc_normal_quantile(u); }
+
 // One path of cell k: start X_i (and its local coordinates), dW, endpoint response Y1.
 template <int D, int P>
 __device__ __forceinline__ void srmc_path(const SrmcDev& s, const double* __restrict__ next, const int* cc,
@@ -192,7 +196,7 @@ __device__ __forceinline__ void srmc_path(const SrmcDev& s, const double* __rest
 #pragma unroll
     for (int l = 0; l < D; ++l) {
         const double u = DMUL(DADD(static_cast<double>(w[D + l] >> 12), 0.5), 0x1p-52);
-        dw[l] = DMUL(s.sqrt_dt, qrmc_normal_quantile(u));
+        dw[l] = DMUL(s.sqrt_dt, srmc_normal_quantile(u));
         x1[l] = DADD(DADD(x0[l], s.bdt), DMUL(s.sig, dw[l]));
     }
     if (s.last) {
