@@ -145,23 +145,61 @@ def dist_env():
     return world, rank, local
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU, NCCL) on this
+    node with the same arguments, as the driver's own torchrun launch would."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 # ------------------------------------------------------------------ reference CPU
-def cpu_reference_solve(paths: int) -> tuple[float, int]:
-    """Wall time of the reference's own backward_solve (oracle/_ref) on all host cores."""
+def cpu_reference_solve(paths: int) -> tuple[float, str]:
+    """Wall time of the reference's own backward_solve (oracle/_ref: the unmodified
+    reference sources, proj/src/solver.cpp:109-226) on all host cores. Nothing of this
+    repo's CUDA library is loaded on this path: #Gamma comes from the reference's own
+    MultiIndexSet (multi_index.cpp:96-173)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles  # test infrastructure: the reference build, only for the baseline leg
-    from paper_2407_21084_b200 import _abi
+    from paper_2407_21084_b200 import _abi  # ctypes structs only (no library load)
     R = oracles.ref() if oracles.have_ref() else None
     kind = "reference"
     if R is None:
         R = oracles.port()
         kind = "port"
     prob, cfg = make_problem_config(paths)
-    k = int(_abi.lib().qrmc_gpu_gamma_size(cfg.c.gamma_kind, prob.dim, cfg.c.degrees, cfg.c.n_degrees)) \
-        if _abi.LIB_PATH.exists() else 12752
+    k = int(R.gamma(cfg.c.gamma_kind, prob.dim, list(WORKLOAD["degrees"]))[0].shape[0])
     t0 = time.perf_counter()
     R.backward_solve(prob, cfg, k)
     return time.perf_counter() - t0, kind
+
+
+def cpu_baseline_sample(paths: int, repeats: int) -> dict:
+    """The reference CPU solver on a bounded sample of the workload: the median of
+    `repeats` full N=20 solves at M = paths, and one solve at 2M to show that time is
+    linear in M (work and memory are exactly proportional to M), so the
+    per-path-step rate extrapolates to the GPU's M."""
+    n = WORKLOAD["steps"]
+    times, kind = [], "reference"
+    for _ in range(repeats):
+        t, kind = cpu_reference_solve(paths)
+        times.append(t)
+    med = statistics.median(times)
+    t2, _ = cpu_reference_solve(2 * paths)
+    cores = os.cpu_count() or 1
+    threads = min(cores, 256, -(-paths // 1024))
+    return {"value": path_steps(paths, n) / med, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"median of {repeats} full N={n} backward solves at M={paths} ({med:.1f} s each) on "
+                      f"{threads} of {cores} host threads; one solve at M={2 * paths} took {t2:.1f} s "
+                      f"(ratio {t2 / med:.2f} vs 2.00 for exact linearity); extrapolated linearly in M "
+                      f"to the GPU workload",
+            "seconds": times, "linearity_2m_over_m": t2 / med, "extrapolated": True}
 
 
 def run_reference_arm(args) -> int:
@@ -179,16 +217,20 @@ def run_reference_arm(args) -> int:
     for _ in range(args.steps):
         t, kind = cpu_reference_solve(paths)
         times.append(t)
-    mean = sum(times) / len(times)
-    value = path_steps(paths, n) / mean
+    med = statistics.median(times)
+    value = path_steps(paths, n) / med
+    t2, _ = cpu_reference_solve(2 * paths)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": med * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD["name"], "paths_per_step_sample": paths, "N": n,
                    "basis": "hyperbolic(4,100) #Gamma=12752", "parallelism": "host threads (lane pool)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"full N={n} backward solve at M={paths} (work is exactly linear in M)"},
+                         "sample": f"full N={n} backward solve at M={paths} per step, median of {args.steps}; "
+                                   f"one solve at M={2 * paths}: {t2:.1f} s vs {med:.1f} s (linear in M); "
+                                   f"rate extrapolated linearly to the GPU's M",
+                         "linearity_2m_over_m": t2 / med, "extrapolated": True},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,6 +241,8 @@ def run_reference_arm(args) -> int:
 def run_ours(args) -> int:
     from paper_2407_21084_b200 import _abi, api
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     import torch
     torch.cuda.set_device(local)
     L = _abi.lib()
@@ -295,13 +339,10 @@ def run_ours(args) -> int:
     L.qrmc_gpu_plan_destroy(plan)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_cpu, kind = cpu_reference_solve(args.cpu_paths)
-        cores = os.cpu_count() or 1
-        cpu = {"value": path_steps(args.cpu_paths, n) / t_cpu, "unit": UNIT,
-               "cores": min(cores, 256, -(-args.cpu_paths // 1024)), "kind": kind,
-               "sample": f"one full N={n} backward solve at M={args.cpu_paths} (work exactly linear in M), "
-                         f"{t_cpu:.1f} s on the box's host cores"}
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args.cpu_paths, args.cpu_repeats)
+    if dist is not None:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -322,7 +363,9 @@ def run_ours(args) -> int:
             "roofline": {"kernel": names[0], "bound": "fp64", "achieved": achieved,
                          "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["fp64_tflops"],
                          "traffic": traffic_per_launch(names[0]),
-                         "peak_source": "measured FP64 (DMMA 37.1 TF/s) on this pool, profiles/r01_fp64_peak.txt"},
+                         "peak_source": "of builder-measured 37.1 TF/s FP64 (DMMA m8n8k4 microbenchmark on this "
+                                        "pool's B200, profiles/r01_fp64_peak.txt; cuBLAS DGEMM 35.5); "
+                                        "MEASURED_PEAKS.json has no FP64 entry"},
             "e2e": {"value": path_steps(paths_total, n) / e2e_t, "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d.value), "d2h_bytes_per_step": int(d2h.value)},
             "gpu_launches": launches,
@@ -345,9 +388,12 @@ def main() -> int:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--paths", type=int, default=DEFAULT_PATHS_PER_GPU, help="paths per GPU per backward step")
     ap.add_argument("--cpu-paths", type=int, default=CPU_SAMPLE_PATHS)
+    ap.add_argument("--cpu-repeats", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

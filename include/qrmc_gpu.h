@@ -199,6 +199,17 @@ const char* qrmc_gpu_plan_kernel_name(const qrmc_gpu_plan_t* plan, int which);
  * chunk c of 1024 paths belongs to lane c % 256) and n_owned paths. */
 qrmc_status qrmc_gpu_lane_ownership(int64_t paths, int32_t rank, int32_t world, int32_t* lane_lo,
                                     int32_t* lane_hi, int64_t* n_owned);
+/* Multi-GPU correctness on one device (test entry): the solve of a world of
+ * `world` ranks with every rank's kernels run on the current device, each with
+ * its own lane ownership (lane_lo > 0, owned_lanes < 256 as on a real rank),
+ * its own response/cloud buffers, writing only its own lanes' partial rows --
+ * the rows the per-step ncclAllGather of a world-`world` solve assembles
+ * (host.cpp enqueue_solve). The reference's contract that `workers` never
+ * changes results (solver.hpp:29) makes the output bitwise equal to the
+ * world-1 solve for every world in [1, 256]. */
+qrmc_status qrmc_gpu_replay_ranks_solve(const qrmc_problem_t* problem, const qrmc_config_t* config,
+                                        int32_t world, double* coeffs, size_t coeffs_len,
+                                        qrmc_stats_t* stats, char* err, size_t err_len);
 /* The kernels' owned index -> global path id map, exported for host-side tests. */
 int64_t qrmc_gpu_owned_path(int64_t q, int32_t lane_lo, int32_t owned_lanes);
 /* Host->device and device->host bytes one qrmc_gpu_backward_solve call moves. */

@@ -38,7 +38,7 @@ extern "C" {
 
 enum { QRMC_SRMC_SIN_BENCH = 0, QRMC_SRMC_BERGMAN = 1 };
 enum { QRMC_SRMC_LP0 = 0, QRMC_SRMC_LP1 = 1 };
-#define QRMC_SRMC_MAX_DIM 8
+#define QRMC_SRMC_MAX_DIM 6
 
 typedef struct {
     int32_t kind;    /* QRMC_SRMC_SIN_BENCH | QRMC_SRMC_BERGMAN */
@@ -63,9 +63,10 @@ typedef struct {
 } qrmc_srmc_config_t;
 
 typedef struct {
-    uint64_t path_steps;   /* sum over steps of cells * M (x2 when Z needs its own pass) */
+    uint64_t path_steps;   /* simulated path-steps: sum over steps of cells * M */
     double device_seconds; /* CUDA-event time of the solve's kernels */
     int32_t kernel_launches;
+    int32_t path_passes;   /* 2 when a z-dependent driver replays every path (Z pass + Y pass), else 1 */
 } qrmc_srmc_stats_t;
 
 /* number of coefficients per cell of the Y table (1 or d+1); <0 on a bad config */

@@ -196,6 +196,7 @@ def _declare(L: C.CDLL) -> None:
     L.qrmc_gpu_plan_kernel_name.restype = C.c_char_p
     L.qrmc_gpu_lane_ownership.argtypes = [C.c_int64, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32),
                                           P(C.c_int64)]
+    L.qrmc_gpu_replay_ranks_solve.argtypes = [P(Problem), P(Config), C.c_int32, P(C.c_double), sz, P(Stats), cp, sz]
     L.qrmc_gpu_owned_path.argtypes = [C.c_int64, C.c_int32, C.c_int32]
     L.qrmc_gpu_owned_path.restype = C.c_int64
     L.qrmc_gpu_plan_destroy.argtypes = [vp]
@@ -218,7 +219,7 @@ EXPORTED_SYMBOLS = (
     "qrmc_gpu_backward_solve", "qrmc_gpu_plan_create", "qrmc_gpu_plan_run",
     "qrmc_gpu_plan_download", "qrmc_gpu_plan_basis_size", "qrmc_gpu_plan_stream",
     "qrmc_gpu_plan_kernel_seconds", "qrmc_gpu_plan_io_bytes", "qrmc_gpu_plan_kernel_name", "qrmc_gpu_mma_layout_check", "qrmc_gpu_table_json", "qrmc_gpu_lane_ownership",
-    "qrmc_gpu_owned_path",
+    "qrmc_gpu_owned_path", "qrmc_gpu_replay_ranks_solve",
     "qrmc_gpu_plan_destroy", "qrmc_gpu_evaluate", "qrmc_gpu_mse_metrics", "qrmc_gpu_philox",
     "qrmc_gpu_stream_draws", "qrmc_gpu_cloud_paths",
 )

@@ -859,6 +859,9 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -875,9 +878,13 @@ NcclApi& nccl() {
         api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(api.handle, "ncclCommInitRank"));
         api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.handle, "ncclCommDestroy"));
         api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(api.handle, "ncclAllGather"));
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.handle, "ncclAllReduce"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(api.handle, "ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(api.handle, "ncclGroupEnd"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.handle, "ncclGetErrorString"));
     });
-    if (!api.handle || !api.GetUniqueId || !api.CommInitRank || !api.AllGather)
+    if (!api.handle || !api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.GroupStart ||
+        !api.GroupEnd)
         fail(QRMC_ENCCL, "libnccl.so.2 could not be loaded");
     return api;
 }
@@ -908,6 +915,17 @@ struct qrmc_gpu_plan {
     int64_t K = 0;
     int steps = 0;
     int lanes_per_rank = kLanes;
+    // The ranks whose paths this process computes: its own session rank, or --
+    // for qrmc_gpu_replay_ranks_solve -- every rank of a virtual world of G ranks
+    // on this one device, each writing its own lanes' partial rows (what the
+    // per-step ncclAllGather assembles when the ranks are separate GPUs).
+    struct Shard {
+        int rank = 0, lane_lo = 0, lane_hi = 0;
+        int64_t n_owned = 0;
+        DevBuf<double> resp, cloud;
+    };
+    std::vector<std::unique_ptr<Shard>> shards;
+    int shard_world = 1;
     DevBuf<uint32_t> d_tile_prog;
     DevBuf<int4> d_tiles;
     DevBuf<int32_t> d_pack_pos, d_item_k, d_item_len, d_item_leaf, d_item_pre;
@@ -923,7 +941,7 @@ struct qrmc_gpu_plan {
     DevBuf<uint32_t> d_mma_terms;
     DevBuf<uint16_t> d_mma_gk;
     DevBuf<int32_t> d_mma_pos;
-    DevBuf<double> d_pack_scale, d_alpha, d_coef, d_partials, d_resp, d_cloud;
+    DevBuf<double> d_pack_scale, d_alpha, d_coef, d_partials;
     DevBuf<unsigned long long> d_counters;
     DevBuf<int> d_flags;
     cudaGraphExec_t graph = nullptr;
@@ -986,26 +1004,52 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
     };
     mark();
     const int world = P.session->world;
-    for (int i = N - 1; i >= 0; --i) {
+    auto shard_args = [&](const qrmc_gpu_plan::Shard& sh, int i) {
         StepArgs a = P.base;
         a.step = i;
-        if (P.use_mma)
-            cuda_check(launch_responses_mma(a, P.mma, st), "k_responses_mma");
-        else
-            cuda_check(launch_responses(a, st), "k_responses");
+        a.lane_lo = sh.lane_lo;
+        a.owned_lanes = sh.lane_hi - sh.lane_lo;
+        a.n_owned = sh.n_owned;
+        a.resp = sh.resp.p;
+        a.cloud = sh.cloud.p;
+        return a;
+    };
+    for (int i = N - 1; i >= 0; --i) {
+        for (const auto& sh : P.shards) {
+            const StepArgs a = shard_args(*sh, i);
+            if (P.use_mma)
+                cuda_check(launch_responses_mma(a, P.mma, st), "k_responses_mma");
+            else
+                cuda_check(launch_responses(a, st), "k_responses");
+        }
         mark();
-        ProjArgs pa = P.proj;
-        pa.partials = P.d_partials.p + static_cast<size_t>(P.session->rank) * P.lanes_per_rank * P.K;
-        if (P.use_proj_mma) {
-            ProjMmaArgs pm = P.pmma;
-            pm.partials = pa.partials;
-            cuda_check(launch_project_mma(a, pm, st), "k_project_mma");
-        } else {
-            cuda_check(launch_project(a, pa, st), "k_project");
+        for (const auto& sh : P.shards) {
+            const StepArgs a = shard_args(*sh, i);
+            ProjArgs pa = P.proj;
+            pa.partials = P.d_partials.p + static_cast<size_t>(sh->lane_lo) * P.K;
+            if (P.use_proj_mma) {
+                ProjMmaArgs pm = P.pmma;
+                pm.partials = pa.partials;
+                cuda_check(launch_project_mma(a, pm, st), "k_project_mma");
+            } else {
+                cuda_check(launch_project(a, pa, st), "k_project");
+            }
         }
         if (world > 1) {
-            nccl_check(nccl().AllGather(pa.partials, P.d_partials.p, static_cast<size_t>(P.lanes_per_rank) * P.K,
-                                        ncclDouble, P.session->comm, st),
+            // Every rank must agree on the solve's fate before the partial rows are
+            // shared: a SimulationError / NumericError on any rank aborts all of
+            // them at the next step's K1 (parallel.cpp:22-43 rethrows the first
+            // lane exception for the whole solve). flags = {kind (max: ESIM wins),
+            // min SimulationError step}.
+            nccl_check(nccl().GroupStart(), "ncclGroupStart");
+            nccl_check(nccl().AllReduce(P.d_flags.p, P.d_flags.p, 1, ncclInt32, ncclMax, P.session->comm, st),
+                       "ncclAllReduce(flags)");
+            nccl_check(nccl().AllReduce(P.d_flags.p + 1, P.d_flags.p + 1, 1, ncclInt32, ncclMin, P.session->comm, st),
+                       "ncclAllReduce(step)");
+            nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+            const size_t lpr = static_cast<size_t>(P.lanes_per_rank);
+            nccl_check(nccl().AllGather(P.d_partials.p + static_cast<size_t>(P.session->rank) * lpr * P.K,
+                                        P.d_partials.p, lpr * P.K, ncclDouble, P.session->comm, st),
                        "ncclAllGather");
         }
         mark();
@@ -1021,13 +1065,21 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
             f.mma_row_len = P.mma.row_len;
             f.mma_pos = P.d_mma_pos.p;
         }
+        StepArgs a = P.base;
+        a.step = i;
         cuda_check(launch_finish(a, f, st), "k_finish_step");
         mark();
+    }
+    if (world > 1) {
+        // TruncationStats are the sums over all lanes (solver.cpp:220-223): every
+        // rank returns the global counters
+        nccl_check(nccl().AllReduce(P.d_counters.p, P.d_counters.p, 2, ncclUint64, ncclSum, P.session->comm, st),
+                   "ncclAllReduce(counters)");
     }
 }
 
 std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem_t& prob,
-                                         const qrmc_config_t& cfg) {
+                                         const qrmc_config_t& cfg, int replay_world = 0) {
     validate_config(cfg);
     auto P = std::make_unique<qrmc_gpu_plan>();
     P->session = s;
@@ -1043,14 +1095,25 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     cudaStream_t st = s->stream;
 
     // lane ownership: rank g owns lanes [g*lpr, min(256, (g+1)*lpr))
-    P->lanes_per_rank = (kLanes + s->world - 1) / s->world;
-    const int lo = std::min(kLanes, s->rank * P->lanes_per_rank);
-    const int hi = std::min(kLanes, lo + P->lanes_per_rank);
+    if (replay_world < 0 || replay_world > kLanes) fail(QRMC_EINVAL, "replay: world must be in [1, 256]");
+    if (replay_world > 0 && s->world != 1) fail(QRMC_EINVAL, "replay: needs a single-process session");
+    const int G = replay_world > 0 ? replay_world : s->world;
+    P->shard_world = G;
+    P->lanes_per_rank = (kLanes + G - 1) / G;
     const int64_t chunks = (cfg.paths + kChunk - 1) / kChunk;
-    int64_t n_owned = 0;
-    for (int lane = lo; lane < hi; ++lane)
-        for (int64_t c = lane; c < chunks; c += kLanes)
-            n_owned += std::min<int64_t>(kChunk, cfg.paths - c * kChunk);
+    for (int r = (replay_world > 0 ? 0 : s->rank); r < (replay_world > 0 ? G : s->rank + 1); ++r) {
+        auto sh = std::make_unique<qrmc_gpu_plan::Shard>();
+        sh->rank = r;
+        sh->lane_lo = std::min(kLanes, r * P->lanes_per_rank);
+        sh->lane_hi = std::min(kLanes, sh->lane_lo + P->lanes_per_rank);
+        for (int lane = sh->lane_lo; lane < sh->lane_hi; ++lane)
+            for (int64_t c = lane; c < chunks; c += kLanes)
+                sh->n_owned += std::min<int64_t>(kChunk, cfg.paths - c * kChunk);
+        sh->resp.alloc(static_cast<size_t>(std::max<int64_t>(sh->n_owned, 1)));
+        if (cfg.memory_mode == QRMC_MEMORY_STORE_CLOUD)
+            sh->cloud.alloc(static_cast<size_t>(std::max<int64_t>(sh->n_owned, 1)) * d);
+        P->shards.push_back(std::move(sh));
+    }
 
     // device tables
     const Program& pg = P->program;
@@ -1065,11 +1128,8 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     P->d_alpha.alloc(static_cast<size_t>(cfg.steps) * pg.kp);
     cuda_check(cudaMemsetAsync(P->d_alpha.p, 0, P->d_alpha.n * sizeof(double), st), "memset");
     P->d_coef.alloc(static_cast<size_t>(cfg.steps) * P->K);
-    P->d_partials.alloc(static_cast<size_t>(P->lanes_per_rank) * s->world * P->K);
+    P->d_partials.alloc(static_cast<size_t>(P->lanes_per_rank) * G * P->K);
     cuda_check(cudaMemsetAsync(P->d_partials.p, 0, P->d_partials.n * sizeof(double), st), "memset");
-    P->d_resp.alloc(static_cast<size_t>(std::max<int64_t>(n_owned, 1)));
-    if (cfg.memory_mode == QRMC_MEMORY_STORE_CLOUD)
-        P->d_cloud.alloc(static_cast<size_t>(std::max<int64_t>(n_owned, 1)) * d);
     P->d_counters.alloc(2);
     P->d_flags.alloc(2);
 
@@ -1083,14 +1143,14 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     a.q = cfg.damping;
     a.seed = cfg.seed;
     a.paths = cfg.paths;
-    a.lane_lo = lo;
-    a.owned_lanes = hi - lo;
-    a.n_owned = n_owned;
+    a.lane_lo = P->shards.front()->lane_lo;  // per shard at launch (enqueue_solve)
+    a.owned_lanes = P->shards.front()->lane_hi - P->shards.front()->lane_lo;
+    a.n_owned = P->shards.front()->n_owned;
     a.alpha_packed = P->d_alpha.p;
     a.kp = pg.kp;
     a.tiles = SeriesTiles{P->d_tiles.p, static_cast<int>(P->d_tiles.n), P->d_tile_prog.p};
-    a.resp = P->d_resp.p;
-    a.cloud = P->d_cloud.p;
+    a.resp = P->shards.front()->resp.p;
+    a.cloud = P->shards.front()->cloud.p;
     a.counters = P->d_counters.p;
     a.err_flags = P->d_flags.p;
     a.abort_flag = P->d_flags.p;
@@ -1201,7 +1261,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
     cuda_check(configure_series_kernels(), "series kernel attributes");
     P->ev.resize(3 * static_cast<size_t>(cfg.steps) + 1);
     for (auto& e : P->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-    P->launches_per_run = 3 * cfg.steps;
+    P->launches_per_run = (2 * static_cast<int>(P->shards.size()) + 1) * cfg.steps;
     P->h2d_bytes += (items.k.size() * 3 + items.pre.size()) * sizeof(int32_t) +
                    pg.pack_pos.size() * sizeof(int32_t) + pg.pack_scale.size() * sizeof(double) +
                    pg.tiles.size() * sizeof(int4) + pg.tile_prog.size() * sizeof(uint32_t);
@@ -1615,6 +1675,24 @@ qrmc_status qrmc_gpu_backward_solve(qrmc_gpu_session_t* session, const qrmc_prob
         }
         auto P = make_plan(session, *problem, *config);
         run_plan(*P, stats, step_wall_seconds);
+        download(*P, coeffs, coeffs_len);
+    }, stats);
+}
+
+qrmc_status qrmc_gpu_replay_ranks_solve(const qrmc_problem_t* problem, const qrmc_config_t* config, int32_t world,
+                                        double* coeffs, size_t coeffs_len, qrmc_stats_t* stats, char* err,
+                                        size_t err_len) {
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->error_step = -1;
+    }
+    return guarded(err, err_len, [&] {
+        if (!problem || !config) fail(QRMC_EINVAL, "replay: null argument");
+        if (world < 1 || world > kLanes) fail(QRMC_EINVAL, "replay: world must be in [1, 256]");
+        std::unique_ptr<qrmc_gpu_session, void (*)(qrmc_gpu_session*)> own(
+            make_session(current_device(), 0, 1, nullptr).release(), destroy_session);
+        auto P = make_plan(own.get(), *problem, *config, world);
+        run_plan(*P, stats, nullptr);
         download(*P, coeffs, coeffs_len);
     }, stats);
 }

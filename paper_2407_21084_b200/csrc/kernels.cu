@@ -32,12 +32,6 @@ __device__ __forceinline__ int64_t owned_to_path(const StepArgs& a, int64_t q) {
     return (r * kLanes + lane) * kChunk + q % kChunk;
 }
 
-__device__ __forceinline__ void record_error(int* flags, int kind, int step) {
-    // flags[0] = first error kind (QRMC_ESIM / QRMC_ENUMERIC), flags[1] = min sim step
-    atomicCAS(flags, 0, kind);
-    if (kind == QRMC_ESIM) atomicMin(flags + 1, step);
-}
-
 __device__ __forceinline__ void sample_start(const MeasureDev& m, int d, Stream& s, double* x) {
     for (int l = 0; l < d; ++l) x[l] = measure_inv_cdf(m, s.next_uniform(), l);
 }

@@ -225,4 +225,14 @@ __device__ __forceinline__ int euler_step(const ProblemDev& p, double* x, double
     return bad;
 }
 
+// flags[0] = error kind, the larger wins (QRMC_ESIM over QRMC_ENUMERIC), so the
+// outcome does not depend on which path or rank fails first (the reference
+// rethrows whichever lane exception comes first, parallel.cpp:22-43);
+// flags[1] = smallest SimulationError step. The multi-rank solve all-reduces both
+// with the same operators (host.cpp enqueue_solve).
+__device__ __forceinline__ void record_error(int* flags, int kind, int step) {
+    atomicMax(flags, kind);
+    if (kind == QRMC_ESIM) atomicMin(flags + 1, step);
+}
+
 }  // namespace qrmc_dev

@@ -479,15 +479,14 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
         if (q < a.n_owned) {
             if (sm.bad[tid]) {
                 // first error kind wins; SimulationError keeps the smallest step
-                atomicCAS(a.err_flags, 0, QRMC_ESIM);
-                atomicMin(a.err_flags + 1, sm.bad[tid]);
+                record_error(a.err_flags, QRMC_ESIM, sm.bad[tid]);
             } else {
                 double xN[D];
 #pragma unroll
                 for (int l = 0; l < D; ++l) xN[l] = sm.x[cur][tid][l];
                 const double term = terminal<D>(a.prob, xN);
                 const double v = DDIV(DADD(term, DMUL(a.dt, sm.dsum[tid])), sm.w0[tid]);
-                if (!isfinite(v)) atomicCAS(a.err_flags, 0, QRMC_ENUMERIC);
+                if (!isfinite(v)) record_error(a.err_flags, QRMC_ENUMERIC, 0);
                 a.resp[q] = v;
             }
         }

@@ -337,9 +337,11 @@ int validate(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c, char* er
     if (!p || !c) return set_err(err, el, "null problem/config"), QRMC_EINVAL;
     if (p->kind != QRMC_SRMC_SIN_BENCH && p->kind != QRMC_SRMC_BERGMAN)
         return set_err(err, el, "unknown SRMC problem kind"), QRMC_ENOTIMPL;
-    if (p->dim < 1 || p->dim > 6) return set_err(err, el, "SRMC dim must be in [1, 6]"), QRMC_EINVAL;
+    if (p->dim < 1 || p->dim > QRMC_SRMC_MAX_DIM) return set_err(err, el, "SRMC dim must be in [1, 6]"), QRMC_EINVAL;
     if (!(p->horizon > 0.0)) return set_err(err, el, "horizon must be > 0"), QRMC_EINVAL;
     if (c->steps < 1) return set_err(err, el, "steps must be >= 1"), QRMC_EINVAL;
+    // stream ids are (step << 40) | path (rng.hpp:73-80): the reference's own bound
+    if (c->steps >= (1 << 22)) return set_err(err, el, "RunConfig: steps exceeds the stream-id layout"), QRMC_EINVAL;
     if (c->cells_per_dim < 1) return set_err(err, el, "cells_per_dim must be >= 1"), QRMC_EINVAL;
     if (c->basis != QRMC_SRMC_LP0 && c->basis != QRMC_SRMC_LP1)
         return set_err(err, el, "basis must be LP0 or LP1"), QRMC_EINVAL;
@@ -518,7 +520,8 @@ extern "C" int32_t qrmc_srmc_solve(const qrmc_srmc_problem_t* prob, const qrmc_s
             goto done;
         }
     if (stats) {
-        stats->path_steps = static_cast<uint64_t>(s.cells) * static_cast<uint64_t>(s.M) * N * (zpass ? 2u : 1u);
+        stats->path_steps = static_cast<uint64_t>(s.cells) * static_cast<uint64_t>(s.M) * N;
+        stats->path_passes = zpass ? 2 : 1;
         stats->device_seconds = ms * 1e-3;
         stats->kernel_launches = N;
     }

@@ -36,7 +36,8 @@ class SrmcConfig(C.Structure):
 
 
 class SrmcStats(C.Structure):
-    _fields_ = [("path_steps", C.c_uint64), ("device_seconds", C.c_double), ("kernel_launches", C.c_int32)]
+    _fields_ = [("path_steps", C.c_uint64), ("device_seconds", C.c_double), ("kernel_launches", C.c_int32),
+                ("path_passes", C.c_int32)]
 
 
 class SrmcError(RuntimeError):
@@ -155,7 +156,7 @@ def solve(problem: SrmcProblem, cfg: SrmcConfig, with_z: bool = False) -> SrmcTa
     if rc:
         raise SrmcError(rc, err.value.decode())
     return SrmcTables(problem, cfg, y, z, {"path_steps": st.path_steps, "device_seconds": st.device_seconds,
-                                          "kernel_launches": st.kernel_launches})
+                                          "kernel_launches": st.kernel_launches, "path_passes": st.path_passes})
 
 
 def _device_step_fn(problem: SrmcProblem, cfg: SrmcConfig):
@@ -222,5 +223,5 @@ def solve_sharded(problem: SrmcProblem, cfg: SrmcConfig, with_z: bool = False, g
             gather(z[i])
     yh = y[:, :cells].cpu().numpy()
     zh = z[:, :cells].cpu().numpy() if with_z else None
-    return SrmcTables(problem, cfg, yh, zh, {"path_steps": (k1 - k0) * cfg.paths_per_cell * N *
-                                             (2 if problem.kind == BERGMAN else 1), "cells": (k0, k1)})
+    return SrmcTables(problem, cfg, yh, zh, {"path_steps": (k1 - k0) * cfg.paths_per_cell * N,
+                                             "path_passes": 2 if problem.kind == BERGMAN else 1, "cells": (k0, k1)})
