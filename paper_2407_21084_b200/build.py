@@ -20,7 +20,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libqrmc_gpu.so"
-SOURCES = [CSRC / "kernels.cu", CSRC / "responses_mma.cu", CSRC / "project_mma.cu", CSRC / "host.cpp",
+SOURCES = [CSRC / "kernels.cu", CSRC / "responses_mma.cu", CSRC / "responses_ws.cu", CSRC / "project_mma.cu", CSRC / "host.cpp",
            CSRC / "table_io.cpp"]
 HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "series_block.cuh", CSRC / "mma_common.cuh", ROOT / "include" / "qrmc_gpu.h",
            ROOT / "include" / "qrmc_normal_quantile.h"]
@@ -83,24 +83,43 @@ def build_srmc(force: bool = False, verbose: bool = False) -> Path:
 
 
 def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """libqrmc_gpu.so: every translation unit compiled for sm_100a in parallel
+    (one nvcc per source), then linked into one shared library in-tree."""
     if out is None:
         build_srmc(force=force, verbose=verbose)
     target = out or OUT
     if out is None and not force and not needs_build():
         return OUT
     target.parent.mkdir(parents=True, exist_ok=True)
-    tmp = target.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{json_include()}",
-           *[f"-D{d}" for d in defines], *map(str, SOURCES), "-o", str(tmp), "-ldl"]
+    objdir = target.parent / ("obj_" + target.stem)
+    objdir.mkdir(parents=True, exist_ok=True)
+    common = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{json_include()}",
+              *[f"-D{d}" for d in defines]]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    r = subprocess.run(cmd, capture_output=True, text=True)
+        common.insert(0, "-Xptxas=-v")
+
+    newest_dep = max(p.stat().st_mtime for p in HEADERS + [Path(__file__)])
+
+    def compile_one(src: Path) -> Path:
+        obj = objdir / (src.name + ".o")
+        if not force and not defines and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, newest_dep):
+            return obj
+        r = subprocess.run([nvcc(), *common, "-c", str(src), "-o", str(obj)], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src.name} ({r.returncode}):\n{r.stderr}")
+        if verbose and r.stderr:
+            print(r.stderr, file=sys.stderr)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    tmp = target.with_suffix(".so.tmp")
+    r = subprocess.run([nvcc(), *ARCH, "-shared", *map(str, objs), "-o", str(tmp), "-ldl"], capture_output=True,
+                       text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr}")
-    if verbose and r.stderr:
-        print(r.stderr, file=sys.stderr)
+        raise RuntimeError(f"nvcc link failed ({r.returncode}):\n{r.stderr}")
     tmp.replace(target)
     return target
 

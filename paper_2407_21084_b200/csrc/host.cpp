@@ -508,8 +508,22 @@ ProjectItems build_project_items(const Gamma& g, const int* offset) {
 // (then lexicographically); for a chain of sets (full, total-degree and
 // hyperbolic index sets) every group is then a prefix of that order, which is
 // checked here -- ok = false sends the plan to the series-program K1.
+#ifndef QRMC_MMA_BANK_ORDER
+#define QRMC_MMA_BANK_ORDER 0
+#endif
+struct MmaLayoutOpts {
+    int warps = kMmaWarps;      // GEMM warps the units are balanced over
+    bool euler_ahead = true;    // the first warps also run the Euler steps (responses_mma.cu)
+    bool ring = true;           // steps aligned to W slots and warp segments to the cp.async ring
+    int bank_order = QRMC_MMA_BANK_ORDER;
+};
+
 struct MmaLayout {
     bool ok = false;
+    // warp-specialised K1 (responses_ws.cu): swizzled [entry][32 paths] table offsets,
+    // relative to the lane's row, per row half (rows 0-3 / 4-7)
+    std::vector<uint4> ws_terms;    // [n_terms][2] byte offsets {sA, sB, bA, bB}
+    std::vector<uint32_t> ws_gk;    // [2][n_groups][d-2] {A | B << 16}
     std::vector<uint32_t> terms;    // [n_terms] table offsets (s | b << 16)
     std::vector<uint16_t> gk;       // [n_groups][d-2] table offsets of the prefix
     std::vector<int4> units;        // {cb0, nb, c0, c1}, warp-contiguous
@@ -523,7 +537,25 @@ struct MmaLayout {
     std::vector<int32_t> proj_out;  // [parts][kProjWarps][kProjTiles][32 lanes][2] -> k, or -1
 };
 
-MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
+// Swizzled table slot of (entry e, path p) in the warp-specialised K1's
+// [entry][32 paths] tables: p ^ (4 (e & 3)), so the 4 distinct entries a
+// half-warp reads (one per lane column) hit 4 distinct 32-byte bank groups
+// whenever they differ mod 4 (the bank-aware term/group order arranges that).
+// For the lane's row block r the value sits at e*32 + 8 (r ^ h) + (row ^ 4 (x & 1)),
+// x = e & 3, h = x >> 1: two base offsets, A (r = 0, 2) and B (r = 1, 3), each
+// relative to the lane's own row; they depend on the row half only.
+inline uint32_t ws_off(int e, int half, bool second) {
+    const int x = e & 3, h = x >> 1;
+    const int rowfix = (x & 1) ? (half ? -4 : 4) : 0;
+    return static_cast<uint32_t>(e * 32 + 8 * (second ? 1 - h : h) + rowfix);
+}
+
+inline int ws_gk_record(int d) { return (2 * (d - 2) + 3) / 4 * 4; }
+inline size_t ws_gk_index(int d, int n_groups, int half, int g, int l) {
+    return (static_cast<size_t>(half) * (n_groups / 2) + g / 2) * ws_gk_record(d) + (g % 2) * (d - 2) + l;
+}
+
+MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpts& opt = MmaLayoutOpts{}) {
     MmaLayout L;
     const int d = g.dim;
     const int64_t K = g.size();
@@ -556,10 +588,7 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     // terms so that their table rows of c_s and of c_b are distinct mod 4 -- the
     // kernels read 4 terms x 4 paths per half-warp from [entry][path] tables with a
     // row stride = 4 (mod 16) banks, so that makes both operand loads conflict-free.
-#ifndef QRMC_MMA_BANK_ORDER
-#define QRMC_MMA_BANK_ORDER 0
-#endif
-    if (QRMC_MMA_BANK_ORDER) {
+    if (opt.bank_order) {
         std::vector<int32_t> out;
         out.reserve(order.size());
         size_t i = 0;
@@ -603,6 +632,15 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     L.terms.assign(static_cast<size_t>(n_terms), row_of(offset[d - 2]) | row_of(offset[d - 1]) << 16);
     for (size_t t = 0; t < order.size(); ++t)
         L.terms[t] = row_of(offset[d - 2] + order[t] / Bn) | row_of(offset[d - 1] + order[t] % Bn) << 16;
+    L.ws_terms.assign(static_cast<size_t>(n_terms) * 2, make_uint4(0u, 0u, 0u, 0u));
+    for (int t = 0; t < n_terms; ++t) {
+        const int pr = t < static_cast<int>(order.size()) ? order[t] : 0;  // padding terms read (0, 0)
+        const int es = offset[d - 2] + pr / Bn, eb = offset[d - 1] + pr % Bn;
+        for (int half = 0; half < 2; ++half)
+            L.ws_terms[static_cast<size_t>(t) * 2 + half] =
+                make_uint4(8 * ws_off(es, half, false), 8 * ws_off(es, half, true), 8 * ws_off(eb, half, false),
+                           8 * ws_off(eb, half, true));
+    }
 
     // groups by size (descending, stable), 8 per column block
     std::vector<int32_t> gi(groups.size());
@@ -611,7 +649,7 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     // Same freedom for groups of equal size: the K1 epilogue reads the prefix
     // rows of groups n = 2 col + h (col = 0..3) of a column block per half-warp,
     // so arrange each such quad to have distinct rows mod 4 on every level.
-    if (QRMC_MMA_BANK_ORDER) {
+    if (opt.bank_order) {
         std::vector<int32_t> out;
         out.reserve(gi.size());
         size_t i = 0;
@@ -647,6 +685,15 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
         for (int l = 0; l < nu; ++l)
             L.gk[static_cast<size_t>(c) * nu + l] = static_cast<uint16_t>(
                 row_of(offset[l] + (c < static_cast<int>(gi.size()) ? at(groups[gi[c]].r0, l) : 0)));
+    // [half][group pair][R]: the two groups of a pair (2 col, 2 col + 1) in one
+    // 16-byte-aligned record of R = 2 (d-2) rounded up to 4 words (ws_gk_index)
+    L.ws_gk.assign(static_cast<size_t>(2) * n_cb * 4 * ws_gk_record(d), 0u);
+    for (int half = 0; half < 2; ++half)
+        for (int c = 0; c < n_cb * 8; ++c)
+            for (int l = 0; l < nu; ++l) {
+                const int e = offset[l] + (c < static_cast<int>(gi.size()) ? at(groups[gi[c]].r0, l) : 0);
+                L.ws_gk[ws_gk_index(d, n_cb * 8, half, c, l)] = ws_off(e, half, false) | ws_off(e, half, true) << 16;
+            }
     std::vector<int32_t> cb_chunks;  // chunks of 4 terms per column block (descending)
     for (int cb = 0; cb < n_cb; ++cb) cb_chunks.push_back(static_cast<int32_t>((groups[gi[8 * cb]].n + 3) / 4));
 
@@ -688,16 +735,18 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     std::vector<int32_t> ui(units.size());
     for (size_t i = 0; i < ui.size(); ++i) ui[i] = static_cast<int32_t>(i);
     std::stable_sort(ui.begin(), ui.end(), [&](int32_t x, int32_t y) { return units[x].cost > units[y].cost; });
-    std::vector<std::vector<int32_t>> per_warp(kMmaWarps);
-    std::vector<double> load(kMmaWarps, 0.0);
+    const int n_warps = opt.warps;
+    std::vector<std::vector<int32_t>> per_warp(n_warps);
+    std::vector<double> load(n_warps, 0.0);
     // the first warps also run the next Euler step and x-only parts during the
     // GEMM phase
 #ifndef QRMC_MMA_EULER_COST
 #define QRMC_MMA_EULER_COST 800
 #endif
     // (responses_mma.cu kAheadThreads: the Euler tasks and the x-only parts)
-    for (int w = 0; w < std::min(kMmaWarps, (std::max(kMmaPaths * d, 3 * kMmaPaths) + 31) / 32); ++w)
-        load[w] = QRMC_MMA_EULER_COST;
+    if (opt.euler_ahead)
+        for (int w = 0; w < std::min(n_warps, (std::max(kMmaPaths * d, 3 * kMmaPaths) + 31) / 32); ++w)
+            load[w] = QRMC_MMA_EULER_COST;
     // Warp w issues on SM sub-partition w % 4, whose DMMA pipe its warps share:
     // balance the four sub-partitions first (LPT), then the warps inside each.
 #ifndef QRMC_MMA_SMSP_BALANCE
@@ -707,7 +756,7 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     std::vector<std::vector<int32_t>> per_sub(kSub);
     {
         std::vector<double> sl(kSub, 0.0);
-        for (int w = 0; w < kMmaWarps; ++w) sl[w % kSub] += load[w];
+        for (int w = 0; w < n_warps; ++w) sl[w % kSub] += load[w];
         for (int32_t u : ui) {
             const int b = static_cast<int>(std::min_element(sl.begin(), sl.end()) - sl.begin());
             per_sub[b].push_back(u);
@@ -717,14 +766,14 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     for (int b = 0; b < kSub; ++b) {
         for (int32_t u : per_sub[b]) {  // still in descending cost order
             int w = b;
-            for (int v = b; v < kMmaWarps; v += kSub)
+            for (int v = b; v < n_warps; v += kSub)
                 if (load[v] < load[w]) w = v;
             per_warp[w].push_back(u);
             load[w] += units[u].cost;
         }
     }
     if (std::getenv("QRMC_DEBUG_LAYOUT")) {
-        for (int w = 0; w < kMmaWarps; ++w) {
+        for (int w = 0; w < n_warps; ++w) {
             std::fprintf(stderr, "warp %2d load %8.0f:", w, load[w]);
             for (int32_t u : per_warp[w])
                 std::fprintf(stderr, " [cb%d nb%d c%d-%d]", units[u].cb0, units[u].nb, units[u].c0, units[u].c1);
@@ -734,7 +783,7 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
     std::vector<int64_t> frag_at(static_cast<size_t>(n_cb) * cb_chunks[0], -1);
     const int cstride = cb_chunks[0];
     int64_t woff = 0;
-    for (int w = 0; w < kMmaWarps; ++w) {
+    for (int w = 0; w < n_warps; ++w) {
         std::sort(per_warp[w].begin(), per_warp[w].end(), [&](int32_t x, int32_t y) {
             return units[x].cb0 != units[y].cb0 ? units[x].cb0 < units[y].cb0 : units[x].c0 < units[y].c0;
         });
@@ -745,13 +794,13 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset) {
             L.units.push_back(make_int4(un.cb0, un.nb, un.c0, un.c1));
             // a step takes 1, 2 or 4 fragment slots (3 column blocks use 4), aligned,
             // so no step straddles the ring wrap
-            const int stride = un.nb == 3 ? 4 : un.nb;
+            const int stride = opt.ring && un.nb == 3 ? 4 : un.nb;
             L.frags += static_cast<int64_t>(un.nb) * (un.c1 - un.c0);
-            f = (f + stride - 1) / stride * stride;
+            if (opt.ring) f = (f + stride - 1) / stride * stride;
             for (int c = un.c0; c < un.c1; ++c, f += stride)
                 for (int i = 0; i < un.nb; ++i) frag_at[static_cast<size_t>(un.cb0 + i) * cstride + c] = woff + f + i;
         }
-        const int64_t fpad = (f + kMmaRingFrags - 1) / kMmaRingFrags * kMmaRingFrags;
+        const int64_t fpad = opt.ring ? (f + kMmaRingFrags - 1) / kMmaRingFrags * kMmaRingFrags : f;
         L.warp_info.push_back(make_int4(ub, static_cast<int>(L.units.size()), static_cast<int>(woff), static_cast<int>(fpad)));
         woff += fpad;
     }
@@ -932,6 +981,12 @@ struct qrmc_gpu_plan {
     int n_items = 0;
     // tensor-core K1 (responses_mma.cu), when the index set allows it
     bool use_mma = false, use_proj_mma = false;
+    bool use_ws = false;  // warp-specialised K1 (responses_ws.cu) in place of k_responses_mma
+    WsArgs ws{};
+    DevBuf<int4> d_ws_units, d_ws_warps;
+    DevBuf<uint4> d_ws_terms;
+    DevBuf<int32_t> d_ws_stride;
+    DevBuf<uint32_t> d_ws_gk;
     MmaArgs mma{};
     ProjMmaArgs pmma{};
     DevBuf<int4> d_pm_rects;
@@ -1017,7 +1072,9 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
     for (int i = N - 1; i >= 0; --i) {
         for (const auto& sh : P.shards) {
             const StepArgs a = shard_args(*sh, i);
-            if (P.use_mma)
+            if (P.use_ws)
+                cuda_check(launch_responses_ws(a, P.ws, st), "k_responses_ws");
+            else if (P.use_mma)
                 cuda_check(launch_responses_mma(a, P.mma, st), "k_responses_mma");
             else
                 cuda_check(launch_responses(a, st), "k_responses");
@@ -1062,8 +1119,9 @@ void enqueue_solve(qrmc_gpu_plan& P, cudaStream_t st, bool with_events) {
         f.pack_scale = P.d_pack_scale.p;
         if (P.use_mma) {
             f.alpha_mma = P.d_alpha_mma.p;
-            f.mma_row_len = P.mma.row_len;
+            f.mma_row_len = P.use_ws ? 0 : P.mma.row_len;
             f.mma_pos = P.d_mma_pos.p;
+            f.mma_stride = P.use_ws ? P.d_ws_stride.p : nullptr;
         }
         StepArgs a = P.base;
         a.step = i;
@@ -1225,6 +1283,67 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                     m.kmax[l] = pa.kmax[l];
                 }
                 cuda_check(configure_responses_mma(d, smem), "k_responses_mma attributes");
+                // the warp-specialised K1 when two table buffers fit (QRMC_K1=mma keeps k_responses_mma)
+                const size_t wsmem = responses_ws_smem_bytes(d, off);
+                if (!(k1 && std::strcmp(k1, "mma") == 0) && wsmem && wsmem <= static_cast<size_t>(optin) &&
+                    static_cast<int64_t>(off) * 32 < 0xFFFF) {
+                    MmaLayoutOpts o;
+                    o.warps = kWsConsumers;
+                    o.euler_ahead = false;
+                    o.ring = false;
+                    o.bank_order = 1;
+                    MmaLayout W = build_mma_layout(P->gamma, pa.offset, o);
+                    if (W.ok) {
+                        P->use_ws = true;
+                        P->d_ws_units.alloc(W.units.size());
+                        P->d_ws_units.upload(W.units.data(), W.units.size(), st);
+                        P->d_ws_warps.alloc(W.warp_info.size());
+                        P->d_ws_warps.upload(W.warp_info.data(), W.warp_info.size(), st);
+                        P->d_ws_terms.alloc(W.ws_terms.size());
+                        P->d_ws_terms.upload(W.ws_terms.data(), W.ws_terms.size(), st);
+                        P->d_ws_gk.alloc(W.ws_gk.size());
+                        P->d_ws_gk.upload(W.ws_gk.data(), W.ws_gk.size(), st);
+                        // warp-major fragment streams: warp w's series 0..N-1 back to back,
+                        // so a consumer (and its L1 prefetch) walks one linear stream from
+                        // alpha_{i+1} to alpha_{N-1}; finish writes alpha_i at pos + i * stride
+                        const int N = cfg.steps;
+                        std::vector<int4> winfo = W.warp_info;
+                        std::vector<int32_t> wpos(W.pos.size()), wstride(W.pos.size());
+                        for (size_t k = 0; k < W.pos.size(); ++k) {
+                            const int64_t frag = W.pos[k] / 32, lane_slot = W.pos[k] % 32;
+                            int w = 0;
+                            while (!(frag >= winfo[w].z && frag < winfo[w].z + winfo[w].w)) ++w;
+                            wpos[k] = static_cast<int32_t>((static_cast<int64_t>(winfo[w].z) * N + (frag - winfo[w].z)) * 32 + lane_slot);
+                            wstride[k] = winfo[w].w * 32;
+                        }
+                        for (auto& wi : winfo) wi.z *= N;
+                        P->d_ws_warps.upload(winfo.data(), winfo.size(), st);
+                        P->d_mma_pos.alloc(wpos.size());
+                        P->d_mma_pos.upload(wpos.data(), wpos.size(), st);
+                        P->d_ws_stride.alloc(wstride.size());
+                        P->d_ws_stride.upload(wstride.data(), wstride.size(), st);
+                        // + the prefetch distance: the last warp's prefetches stay in bounds
+                        P->d_alpha_mma.alloc(static_cast<size_t>(N) * W.row_len + 32 * (kWsPrefetch + 2));
+                        cuda_check(cudaMemsetAsync(P->d_alpha_mma.p, 0, P->d_alpha_mma.n * sizeof(double), st), "memset");
+                        m.alpha = nullptr;  // k_responses_mma is not launched
+                        WsArgs& w = P->ws;
+                        w.alpha = P->d_alpha_mma.p;
+                        w.units = P->d_ws_units.p;
+                        w.warp_info = P->d_ws_warps.p;
+                        w.terms = P->d_ws_terms.p;
+                        w.gk = P->d_ws_gk.p;
+                        w.n_groups = static_cast<int>(W.ws_gk.size() / ws_gk_record(d));
+                        w.table_len = off;
+                        for (int l = 0; l < d; ++l) {
+                            w.offset[l] = pa.offset[l];
+                            w.kmax[l] = pa.kmax[l];
+                        }
+                        cuda_check(configure_responses_ws(d, wsmem), "k_responses_ws attributes");
+                        P->h2d_bytes += (W.units.size() + W.warp_info.size()) * sizeof(int4) +
+                                        W.ws_terms.size() * sizeof(uint4) + W.ws_gk.size() * sizeof(uint32_t) +
+                                        2 * W.pos.size() * sizeof(int32_t);
+                    }
+                }
                 // K2 on the tensor cores (QRMC_K2=series forces the series K2)
                 const char* k2 = std::getenv("QRMC_K2");
                 const size_t psmem = project_mma_smem_bytes(off);
@@ -1511,6 +1630,98 @@ qrmc_status qrmc_gpu_mma_layout_check(int32_t kind, int32_t dim, const int32_t* 
             e2 = std::max(e2, std::fabs(part[static_cast<size_t>(r)] - term(r)));
         }
         *max_rel_err = std::max(std::fabs(y - direct) / std::max(scale, 1e-300), e2);
+        // warp-specialised K1 (responses_ws.cu): 32 paths with their own points in
+        // swizzled [entry][32] tables; replay every lane's operand addressing
+        // (row-half offsets, row blocks r = 0..3 at A[0], B[0], A[16], B[16]) and the
+        // dense per-warp fragment streams, then compare each path's y with the direct sum
+        {
+            MmaLayoutOpts o;
+            o.warps = kWsConsumers;
+            o.euler_ahead = false;
+            o.ring = false;
+            o.bank_order = 1;
+            const MmaLayout W = build_mma_layout(g, offset, o);
+            if (!W.ok) fail(QRMC_ELOGIC, "ws layout: not a chain although the mma layout is");
+            std::vector<double> wtab(static_cast<size_t>(off) * 32, 0.0);
+            std::vector<std::vector<double>> ptab(32, std::vector<double>(static_cast<size_t>(off), 0.0));
+            for (int p = 0; p < 32; ++p)
+                for (int l = 0; l < d; ++l) {
+                    const double th = 3.141592653589793 * rnd();
+                    for (int k = 0; k <= g.kmax[l]; ++k) {
+                        const int e = offset[l] + k;
+                        const double v = std::cos(k * th);
+                        ptab[p][static_cast<size_t>(e)] = v;
+                        wtab[static_cast<size_t>(e) * 32 + (p ^ ((e & 3) << 2))] = v;
+                    }
+                }
+            std::vector<double> ws(static_cast<size_t>(W.row_len), 0.0);
+            std::vector<uint8_t> whit(static_cast<size_t>(W.row_len), 0);
+            for (int64_t r = 0; r < K; ++r) {
+                const int32_t q = W.pos[static_cast<size_t>(r)];
+                if (q < 0 || q >= W.row_len || whit[static_cast<size_t>(q)]) fail(QRMC_ELOGIC, "ws layout: position clash");
+                whit[static_cast<size_t>(q)] = 1;
+                ws[static_cast<size_t>(q)] = alpha[static_cast<size_t>(r)];
+            }
+            const int n_groups = static_cast<int>(W.ws_gk.size() / ws_gk_record(d));  // 2 halves x n/2 pairs
+            auto at_off = [&](int lane, uint32_t o16, int r16) {  // the kernel's trow + o16 + 16 r16
+                return wtab[static_cast<size_t>((lane >> 2) + static_cast<int>(o16) + 16 * r16)];
+            };
+            std::vector<double> yp(32, 0.0);
+            for (int w = 0; w < kWsConsumers; ++w) {
+                const int4 wi = W.warp_info[static_cast<size_t>(w)];
+                int64_t f = wi.z;
+                for (int u = wi.x; u < wi.y; ++u) {
+                    const int4 un = W.units[static_cast<size_t>(u)];
+                    const int nb = un.y;
+                    std::vector<double> C(static_cast<size_t>(nb) * 4 * 64, 0.0);  // [i][r][path row][group col]
+                    for (int c = un.z; c < un.w; ++c, f += nb)
+                        for (int i = 0; i < nb; ++i)
+                            for (int lane = 0; lane < 32; ++lane) {
+                                // A[row][k] for row blocks r: this lane's (row, col = k) value
+                                const int row = lane >> 2, col = lane & 3, half = row >> 2;
+                                const uint4 tw = W.ws_terms[static_cast<size_t>(4 * c + col) * 2 + half];
+                                double a[4];
+                                a[0] = at_off(lane, tw.x / 8, 0) * at_off(lane, tw.z / 8, 0);
+                                a[1] = at_off(lane, tw.y / 8, 0) * at_off(lane, tw.w / 8, 0);
+                                a[2] = at_off(lane, tw.x / 8, 1) * at_off(lane, tw.z / 8, 1);
+                                a[3] = at_off(lane, tw.y / 8, 1) * at_off(lane, tw.w / 8, 1);
+                                for (int r = 0; r < 4; ++r)
+                                    for (int n = 0; n < 8; ++n)  // B[k = col][n] sits at lane n * 4 + col
+                                        C[((static_cast<size_t>(i) * 4 + r) * 8 + row) * 8 + n] +=
+                                            a[r] * ws[static_cast<size_t>((f + i) * 32 + n * 4 + col)];
+                            }
+                    for (int i = 0; i < nb; ++i)
+                        for (int lane = 0; lane < 32; ++lane) {
+                            const int row = lane >> 2, col = lane & 3, half = row >> 2;
+                            const int g0 = 8 * (un.x + i) + 2 * col;
+                            for (int h = 0; h < 2; ++h) {
+                                double uu[4] = {1, 1, 1, 1};
+                                for (int l = 0; l < d - 2; ++l) {
+                                    const uint32_t o = W.ws_gk[ws_gk_index(d, n_groups, half, g0 + h, l)];
+                                    uu[0] *= at_off(lane, o & 0xFFFFu, 0);
+                                    uu[1] *= at_off(lane, o >> 16, 0);
+                                    uu[2] *= at_off(lane, o & 0xFFFFu, 1);
+                                    uu[3] *= at_off(lane, o >> 16, 1);
+                                }
+                                for (int r = 0; r < 4; ++r)
+                                    yp[static_cast<size_t>(8 * r + row)] +=
+                                        uu[r] * C[((static_cast<size_t>(i) * 4 + r) * 8 + row) * 8 + 2 * col + h];
+                            }
+                        }
+                }
+                if (f != wi.z + wi.w) fail(QRMC_ELOGIC, "ws layout: warp stream length mismatch");
+            }
+            for (int p = 0; p < 32; ++p) {
+                double dp = 0.0, sp = 0.0;
+                for (int64_t r = 0; r < K; ++r) {
+                    double v = alpha[static_cast<size_t>(r)];
+                    for (int l = 0; l < d; ++l) v *= ptab[p][static_cast<size_t>(offset[l] + g.rows[static_cast<size_t>(r * d + l)])];
+                    dp += v;
+                    sp += std::fabs(v);
+                }
+                *max_rel_err = std::max(*max_rel_err, std::fabs(yp[static_cast<size_t>(p)] - dp) / std::max(sp, 1e-300));
+            }
+        }
         info[1] = K;
         info[2] = static_cast<int64_t>(L.units.size());
         info[3] = L.frags;
@@ -1631,7 +1842,7 @@ qrmc_status qrmc_gpu_plan_io_bytes(const qrmc_gpu_plan_t* plan, uint64_t* h2d, u
 const char* qrmc_gpu_plan_kernel_name(const qrmc_gpu_plan_t* plan, int which) {
     if (!plan) return nullptr;
     switch (which) {
-        case 0: return plan->use_mma ? "k_responses_mma" : "k_responses";
+        case 0: return plan->use_ws ? "k_responses_ws" : plan->use_mma ? "k_responses_mma" : "k_responses";
         case 1: return plan->use_proj_mma ? "k_project_mma" : "k_project";
         case 2: return "k_finish_step";
         default: return nullptr;

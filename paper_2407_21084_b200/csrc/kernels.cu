@@ -342,7 +342,8 @@ __global__ void k_finish_step(const StepArgs a, const FinishArgs f) {
     f.coef_row[k] = v;
     const double scaled = DMUL(v, f.pack_scale[k]);
     a.alpha_packed[static_cast<int64_t>(a.step) * a.kp + f.pack_pos[k]] = scaled;
-    if (f.alpha_mma) f.alpha_mma[static_cast<int64_t>(a.step) * f.mma_row_len + f.mma_pos[k]] = scaled;
+    if (f.alpha_mma)
+        f.alpha_mma[static_cast<int64_t>(a.step) * (f.mma_stride ? f.mma_stride[k] : f.mma_row_len) + f.mma_pos[k]] = scaled;
 }
 
 // ---------------------------------------------------------------- probes

@@ -87,6 +87,31 @@ struct MmaArgs {
     int kmax[kMaxDim];
 };
 
+// K1, warp-specialised (responses_ws.cu): kWsConsumers warps run the staircase
+// GEMM of evaluation j from one of two cosine-table buffers while kWsProducers
+// warps run the Euler steps, the x-only parts, the truncation/driver of
+// evaluation j-2 and the tables of evaluation j+1 into the other buffer; the
+// hand-off uses named barriers. B fragments stream from L2 (prefetched to L1).
+constexpr int kWsConsumers = 16;
+constexpr int kWsProducers = 4;
+constexpr int kWsPaths = 32;    // paths per CTA (4 row blocks of 8)
+#ifndef QRMC_WS_PREFETCH
+#define QRMC_WS_PREFETCH 4
+#endif
+constexpr int kWsPrefetch = QRMC_WS_PREFETCH;  // fragments the L1 prefetch runs ahead
+
+struct WsArgs {
+    const double* alpha;      // fragment streams, warp-major: warp w's series 0..N-1 back to back
+    const int4* units;        // {cb0, nb, c0, c1}, warp-contiguous
+    const int4* warp_info;    // [kWsConsumers] {unit_begin, unit_end, first fragment of series 0, frags per series}
+    const uint4* terms;       // [n_terms][2 row halves] swizzled byte offsets {sA, sB, bA, bB}
+    const uint32_t* gk;       // [2 row halves][n_groups / 2 pairs][R = 2 (D-2) up to 4k] swizzled offsets {A | B << 16}
+    int n_groups;             // groups, padded to whole column blocks
+    int table_len;            // table entries (all coordinates)
+    int offset[kMaxDim];
+    int kmax[kMaxDim];
+};
+
 // K2 on the FP64 tensor cores (project_mma.cu): per owned lane, the staircase
 // G[u][t] = sum_m S_m U_u(X_m) A_t(X_m) as mma.m8n8k4.f64 (8 groups x 8 terms x
 // 4 paths); each warp keeps one rectangle of <= kProjTiles output tiles in
@@ -140,7 +165,8 @@ struct FinishArgs {
     const double* pack_scale;    // sqrt2^{nnz(k)}
     double* alpha_mma;           // [N][mma_row_len] fragment stream, or nullptr
     int64_t mma_row_len;
-    const int32_t* mma_pos;      // k -> fragment-stream position
+    const int32_t* mma_pos;      // k -> fragment-stream position of series 0
+    const int32_t* mma_stride;   // k -> distance between series (nullptr: mma_row_len)
 };
 
 cudaError_t configure_series_kernels();  // once per process, before the first series launch
@@ -148,6 +174,9 @@ cudaError_t launch_responses(const StepArgs& a, cudaStream_t st);
 size_t responses_mma_smem_bytes(int dim, int table_len);
 cudaError_t configure_responses_mma(int dim, size_t smem);
 cudaError_t launch_responses_mma(const StepArgs& a, const MmaArgs& m, cudaStream_t st);
+size_t responses_ws_smem_bytes(int dim, int table_len);
+cudaError_t configure_responses_ws(int dim, size_t smem);
+cudaError_t launch_responses_ws(const StepArgs& a, const WsArgs& m, cudaStream_t st);
 size_t project_smem_bytes(const ProjArgs& p);
 cudaError_t configure_project(int dim, size_t smem);
 cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st);

@@ -66,3 +66,25 @@ def test_cxx_wrapper_accepts_reference_types(tmp_path):
     src.write_text(WITH_REF)
     subprocess.run([_gxx(), "-std=gnu++20", "-fsyntax-only", f"-I{ROOT / 'include'}", f"-I{REF_INC}",
                     str(src)], check=True)
+
+
+DROPIN = ROOT / "oracle" / "_ref" / "dropin_check"
+
+
+@pytest.mark.gpu
+def test_reference_call_site_runs_the_dropin_on_the_device():
+    """oracle/dropin_check.cpp: a reference call site compiled against the reference's own
+    headers and sources (oracle/Makefile, in the build container) with include/qrmc_gpu.hpp
+    (QRMC_GPU_WITH_REFERENCE_TYPES), linked against libqrmc_gpu.so: the acceptance
+    determinism criterion (acceptance_main.cpp:369-395) through the drop-in, its
+    CoefficientTable against qrmc::backward_solve on the same inputs (1e-10, TruncationStats
+    equal) and the same exception types/messages/steps as the reference."""
+    import torch
+    assert torch.cuda.is_available()
+    if not DROPIN.exists():
+        pytest.skip("oracle/_ref/dropin_check not built (needs /root/reference at build time)")
+    out = subprocess.run([str(DROPIN)], capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "DROPIN OK" in out.stdout
+    assert out.stdout.count("PASS") >= 10 and "FAIL" not in out.stdout

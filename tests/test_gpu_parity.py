@@ -273,7 +273,32 @@ def test_series_program_kernels_match_reference(L, entry, monkeypatch):
 def test_tensor_core_kernels_selected(L, dim, kind, deg):
     prob = _abi.sin_bench_problem(dim)
     cfg = _abi.ConfigHolder(steps=3, paths=2048, damping=5.1, seed=1, gamma_kind=kind, degrees=deg)
-    assert _kernel_names(prob, cfg) == ["k_responses_mma", "k_project_mma", "k_finish_step"]
+    assert _kernel_names(prob, cfg) == ["k_responses_ws", "k_project_mma", "k_finish_step"]
+
+
+@pytest.mark.parametrize("entry", [e for e in GOLDEN["solves"] if e["case"]["dim"] >= 3],
+                         ids=lambda e: e["case"]["name"])
+def test_ring_tensor_core_k1_matches_reference(L, entry, monkeypatch):
+    # QRMC_K1=mma keeps the single-buffered k_responses_mma (cp.async fragment
+    # rings) that the warp-specialised K1 replaced; both must reproduce the goldens
+    case = entry["case"]
+    prob, cfg = build_case(case)
+    monkeypatch.setenv("QRMC_K1", "mma")
+    assert _kernel_names(prob, cfg)[0] == "k_responses_mma"
+    coeffs, stats, _ = api.backward_solve(prob, cfg)
+    ref = unhex(entry["coeffs"]).reshape(coeffs.shape)
+    assert alpha_close(coeffs, ref) <= ALPHA_TOL
+    assert (stats.applications, stats.clipped) == (entry["applications"], entry["clipped"])
+
+
+def test_ws_and_ring_k1_agree_at_config2_shape(L, monkeypatch):
+    prob = _abi.sin_bench_problem(4)
+    cfg = _abi.ConfigHolder(steps=6, paths=40_000, damping=5.1, seed=3, gamma_kind=2, degrees=[100])
+    a, sa, _ = api.backward_solve(prob, cfg)
+    monkeypatch.setenv("QRMC_K1", "mma")
+    b, sb, _ = api.backward_solve(prob, cfg)
+    assert alpha_close(a, b) <= ALPHA_TOL
+    assert (sa.applications, sa.clipped) == (sb.applications, sb.clipped)
 
 
 def test_tensor_core_and_series_kernels_agree(L):
