@@ -82,7 +82,7 @@ def build_srmc(force: bool = False, verbose: bool = False) -> Path:
     return SRMC_OUT
 
 
-def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=(), only=None) -> Path:
     """libqrmc_gpu.so: every translation unit compiled for sm_100a in parallel
     (one nvcc per source), then linked into one shared library in-tree."""
     if out is None:
@@ -102,6 +102,10 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
     newest_dep = max(p.stat().st_mtime for p in HEADERS + [Path(__file__)])
 
     def compile_one(src: Path) -> Path:
+        if only is not None and src.name not in only:
+            # a variant build recompiles only `only`; the rest come from the main build
+            build(verbose=verbose)
+            return OUT.parent / ("obj_" + OUT.stem) / (src.name + ".o")
         obj = objdir / (src.name + ".o")
         if not force and not defines and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, newest_dep):
             return obj

@@ -70,6 +70,13 @@ __device__ __forceinline__ long long clk() {
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
     return t;
 }
+// clock read ordered after the value v is available (v read from shared memory
+// after a barrier: the barrier's completion, which bar.sync may defer)
+__device__ __forceinline__ long long clk_dep(double v) {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : "d"(v) : "memory");
+    return t;
+}
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 // read-only loads with an L1 eviction priority: the operand tables (terms, group
 // rows, units; re-read every evaluation) stay, the streamed B fragments go first
@@ -174,15 +181,26 @@ __device__ __forceinline__ void ws_unit(const WsArgs& m, int cb0, int c0, int c1
         const double* bA = reinterpret_cast<const double*>(trow + cw.z);
         const double* bB = reinterpret_cast<const double*>(trow + cw.w);
         double a[kRB];
+#ifdef QRMC_WS_EXP_NODMUL  // timing experiments only (wrong results)
+        a[0] = sA[0];
+        a[1] = sB[0];
+        a[2] = bA[16];
+        a[3] = bB[16];
+#else
         a[0] = DMUL(sA[0], bA[0]);
         a[1] = DMUL(sB[0], bB[0]);
         a[2] = DMUL(sA[16], bA[16]);
         a[3] = DMUL(sB[16], bB[16]);
+#endif
         double b[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
+#ifdef QRMC_WS_EXP_NOB
+            b[i] = static_cast<double>(col + i);
+#else
             b[i] = ldg_stream(bsrc + 32 * i);
             prefetch_l1(bsrc + 32 * (kWsPrefetch + i));
+#endif
         }
         bsrc += 32 * NB;
 #pragma unroll
@@ -205,6 +223,13 @@ __device__ __forceinline__ void ws_unit(const WsArgs& m, int cb0, int c0, int c1
     }
     for (; c < c1; ++c) step(std::false_type{}, c + 1 < c1);
     // epilogue: groups g0 = 8 (cb0 + i) + 2 col + h, U = prod_{l < D-2} c_{k_l}
+#ifdef QRMC_WS_EXP_NOEPI
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int r = 0; r < kRB; ++r) y[r] += acc[r][i][0] + acc[r][i][1] + wp[i][0];
+    return;
+#endif
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
 #pragma unroll
@@ -273,10 +298,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             const long long t0 = clk();
 #endif
             bar_sync(kBarFull + (j & 1), kFullCount);
-#ifdef QRMC_WS_CLOCKS
-            const long long t1 = clk();
-#endif
             const char* trow = reinterpret_cast<const char*>(tabs + (j & 1) * tab_elems + row);
+#ifdef QRMC_WS_CLOCKS
+            const long long t1 = clk_dep(*reinterpret_cast<const volatile double*>(trow));
+#endif
             for (int u = wi.x; u < wi.y; ++u) {
                 const int4 un = ldg_keep(&m.units[u]);
                 if (un.y == 1)
@@ -294,13 +319,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
 #ifdef QRMC_WS_CLOCKS
             cts[j][0] = t0;
             cts[j][1] = t1;
-            cts[j][2] = clk();
+            cts[j][2] = clk_dep(y[0]);
 #endif
         }
 #ifdef QRMC_WS_CLOCKS
         if ((blockIdx.x == 1000 || blockIdx.x == 30000) && lane == 0 && (cw % 4 == 0))
             for (int j = i0; j < N - 1; ++j)
-                printf("B%d C%d j=%d full_at=%lld wait=%lld gemm=%lld\n", blockIdx.x, cw, j, cts[j][0], cts[j][1] - cts[j][0], cts[j][2] - cts[j][1]);
+                printf("B%d C%d j=%d wait=%lld gemm=%lld\n", blockIdx.x, cw, j, cts[j][1] - cts[j][0], cts[j][2] - cts[j][1]);
 #endif
         return;
     }
@@ -363,9 +388,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
     for (int j = i0; j < N; ++j) {
         // Euler step j (sde.cpp:37-73): X_{j+1} from X_j, draw D + (j-i)*D + l
         const int src = (j - i0) & 1;
+#ifdef QRMC_WS_CLOCKS
+        const long long estart = clk();
+#endif
         for (int l = pw; l < D; l += kWsProducers) {
+#ifndef QRMC_WS_EXP_NOEULER
             const double nrm = qrmc_normal_quantile(
                 u64_to_uniform(stream_u64_at(a.seed, sid, static_cast<uint64_t>(D) * (j - i0 + 1) + l)));
+#else
+            const double nrm = 0.001 * (j + l);
+#endif
             const double dw = DMUL(a.sqrt_dt, nrm);
             const double out = a.prob.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(a.prob.sigma, dw) : dw;
             const double xo = sm.x[src][p][l];
@@ -375,11 +407,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[p] == 0) sm.bad[p] = j + 1;
         }
 #ifdef QRMC_WS_CLOCKS
-        const long long e0 = clk();
+        const long long e0 = clk_dep(sm.x[src ^ 1][p][pw]);  // Euler done (own value)
 #endif
         bar_sync(kBarProd, kProdThreads);
 #ifdef QRMC_WS_CLOCKS
-        const long long e1 = clk();
+        const long long e1 = clk_dep(*reinterpret_cast<volatile double*>(&sm.x[src ^ 1][p][(pw + 1) % D]));
 #endif
         if (pw == 0) {
             // the GEMM of evaluation j-2 has released table buffer j & 1
@@ -404,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             }
         }
 #ifdef QRMC_WS_CLOCKS
-        const long long e2 = clk();
+        const long long e2 = clk_dep(pw == 0 ? 0.0 : (pw == 1 ? sm.wq[j % 3][p] : pw == 2 ? sm.lq[j % 3][p] : sm.dpre[j % 3][p]));
 #endif
         if (j + 1 < N) {
             // cosine tables of evaluation j (X_{j+1}) into buffer j & 1
@@ -412,15 +444,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             double* tb = tabs + (j & 1) * tab_elems;
             for (int l = pw; l < D; l += kWsProducers) {
                 const double th = DMUL(3.14159265358979323846, measure_cdf(a.meas, sm.x[src ^ 1][p][l], l));
+#ifndef QRMC_WS_EXP_NOTAB
                 ws_table(th, m.kmax[l], m.offset[l], p, tb);
+#else
+                if (th == 12345.0) tb[p] = th;
+#endif
             }
             bar_arrive(kBarFull + (j & 1), kFullCount);
         }
 #ifdef QRMC_WS_CLOCKS
-        pts[j][0] = e0;
-        pts[j][1] = e1;
-        pts[j][2] = e2;
-        pts[j][3] = clk();
+        pts[j][0] = e0 - estart;   // Euler compute (incl. iteration start)
+        pts[j][1] = e1 - e0;       // wait for the other producers' Euler
+        pts[j][2] = e2 - e1;       // parts (warps 1-3) / DONE wait (warp 0)
+        pts[j][3] = clk_dep(*reinterpret_cast<volatile double*>(tabs + (j & 1) * tab_elems + p)) - e2;  // sync + tables
 #endif
         // truncation + driver of evaluation j-2 off the tables' critical path: its
         // partial sums sit in slot (j-2) % 3, which the consumers rewrite only after
@@ -437,8 +473,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
 #ifdef QRMC_WS_CLOCKS
     if ((blockIdx.x == 1000 || blockIdx.x == 30000) && p == 0)
         for (int j = i0; j < N; ++j)
-            printf("B%d P%d j=%d start=%lld euler_end=%lld sync1=%lld parts=%lld tables=%lld\n", blockIdx.x, pw, j,
-                   pstart, pts[j][0], pts[j][1] - pts[j][0], pts[j][2] - pts[j][1], pts[j][3] - pts[j][2]);
+            printf("B%d P%d j=%d euler=%lld sync1=%lld parts=%lld tables=%lld\n", blockIdx.x, pw, j,
+                   pts[j][0], pts[j][1], pts[j][2], pts[j][3]);
 #endif
     bar_sync(kBarProd, kProdThreads);  // the terminal parts (warps 1-3) are in place
     if (pw != 0) return;
