@@ -237,6 +237,83 @@ def run_reference_arm(args) -> int:
     return 0
 
 
+# ------------------------------------------------------------------ SRMC (row f3)
+# The north_star's stratified regression Monte Carlo solver at the literal BASELINE.json
+# configs 2 and 4 (include/qrmc_srmc.h; no reference arm: the reference has no SRMC).
+# Hypercubes are partitioned over the ranks and every step's table is all-gathered
+# (strong scaling: the cell count is the config's, whatever N).
+SRMC_WORKLOADS = {
+    "config2": ("sin-d4-lp1-40^4-N20-M1000", 4, dict(steps=20, cells_per_dim=40, paths_per_cell=1000, basis=1)),
+    "config4": ("sin-d6-lp0-16^6-N10-M100", 6, dict(steps=10, cells_per_dim=16, paths_per_cell=100, basis=0)),
+}
+DFMA_PEAK_TFLOPS = 34.2  # builder-measured scalar DFMA peak (profiles/r01_fp64_peak.txt); SRMC runs no tensor op
+
+
+def srmc_flops_per_path_step(d: int, P: int) -> int:
+    """Floating-point operations the SRMC scheme performs per path-step (one cell path, one
+    Euler step), counted from its specification (include/qrmc_srmc.h, oracle/srmc_oracle.c):
+    start point 3d + basis 2d; d AS241 normal quantiles at 35 each (two degree-7 rational
+    polynomials = 28 FMA-flops, division, log, sqrt, scaling); Euler 3d + 1d (sqrt(dt) z);
+    projection + cell + local coordinates 7d; local polynomial 2P; SinBenchmark driver
+    d + 7 (sin counted once); truncation 0; normal equations P(P+1) (packed Gram, FMA) and
+    right-hand side 2 + 2P. RNG integer work is not counted."""
+    return 5 * d + 35 * d + 4 * d + 7 * d + 2 * P + (d + 7) + P * (P + 1) + 2 + 2 * P
+
+
+def run_srmc(args, world: int, rank: int, local: int, dist) -> dict:
+    import torch
+    from paper_2407_21084_b200 import srmc
+    out = {}
+    for key, (name, d, kw) in SRMC_WORKLOADS.items():
+        p, c = srmc.sin_bench_problem(d), srmc.config(**kw)
+        nid = None
+        if world > 1:
+            obj = [srmc.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
+        plan = srmc.SrmcPlan(p, c, local, rank, world, nid)
+        for _ in range(args.srmc_warmup):
+            plan.run()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        dev = []
+        with ClockSampler(local) as clocks:
+            for _ in range(args.srmc_steps):
+                dev.append(plan.run()["device_seconds"])
+        t = statistics.median(dev)
+        if dist is not None:
+            tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        plan.close()
+        cells = kw["cells_per_dim"] ** d
+        ps = cells * kw["paths_per_cell"] * kw["steps"]  # whole job (all ranks)
+        P = d + 1 if kw["basis"] == 1 else 1
+        fl = srmc_flops_per_path_step(d, P)
+        entry = {"workload": name, "value": ps / t, "unit": "path-steps/s", "seconds_per_solve": t,
+                 "cells": cells, "paths_per_cell": kw["paths_per_cell"], "N": kw["steps"], "basis": f"LP{kw['basis']}",
+                 "n_gpus": world, "scaling": "strong (fixed hypercubes, partitioned over the ranks)",
+                 "exchange": "ncclAllGather of every step's y table" if world > 1 else "none (1 rank)",
+                 "clocks": clocks.summary(),
+                 "roofline": {"bound": "fp64", "flops_per_path_step": fl,
+                              "achieved": ps * fl / t / 1e12 / world, "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": ps * fl / t / 1e12 / world / DFMA_PEAK_TFLOPS,
+                              "peak_source": "of builder-measured scalar DFMA 34.2 TF/s (profiles/r01_fp64_peak.txt)",
+                              "note": "per GPU; path generation (Philox, AS241 quantiles) dominates; HBM traffic "
+                                      "per path-step is ~2P*8/M bytes (table read + write), far below the ridge"}}
+        if world == 1:
+            # e2e: the public one-shot call with host tables (allocation, solve, D2H of every step's table)
+            t0 = time.perf_counter()
+            tab = srmc.solve(p, c)
+            e2e = time.perf_counter() - t0
+            entry["e2e"] = {"value": ps / e2e, "unit": "path-steps/s", "h2d_bytes_per_step": 0,
+                            "d2h_bytes_per_step": int(tab.y.nbytes)}
+            del tab
+        out[key] = entry
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args) -> int:
     from paper_2407_21084_b200 import _abi, api
@@ -338,6 +415,7 @@ def run_ours(args) -> int:
     names = [L.qrmc_gpu_plan_kernel_name(plan, w).decode() for w in range(3)]
     L.qrmc_gpu_plan_destroy(plan)
 
+    srmc_line = None if args.no_srmc else run_srmc(args, world, rank, local, dist)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(args.cpu_paths, args.cpu_repeats)
@@ -373,6 +451,8 @@ def run_ours(args) -> int:
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if srmc_line is not None:
+            line["srmc"] = srmc_line
         print(json.dumps(line), flush=True)
     L.qrmc_gpu_session_destroy(session)
     if dist is not None:
@@ -389,6 +469,9 @@ def main() -> int:
     ap.add_argument("--paths", type=int, default=DEFAULT_PATHS_PER_GPU, help="paths per GPU per backward step")
     ap.add_argument("--cpu-paths", type=int, default=CPU_SAMPLE_PATHS)
     ap.add_argument("--cpu-repeats", type=int, default=3)
+    ap.add_argument("--no-srmc", action="store_true", help="skip the SRMC (row f3) section")
+    ap.add_argument("--srmc-steps", type=int, default=3)
+    ap.add_argument("--srmc-warmup", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -73,9 +73,9 @@ typedef struct {
 int32_t qrmc_srmc_basis_size(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg);
 /* n^d; <0 on a bad config */
 int64_t qrmc_srmc_cells(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg);
-/* Full backward solve on the current CUDA device. y: steps * cells * P doubles (host),
- * z: steps * cells * d * P doubles or NULL. Returns 0 or a qrmc_status code with a
- * message in err. */
+/* Full backward solve on the current CUDA device (a world-1 plan: create, run,
+ * download, destroy). y: steps * cells * P doubles (host), z: steps * cells * d * P
+ * doubles or NULL. Returns 0 or a qrmc_status code with a message in err. */
 int32_t qrmc_srmc_solve(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, double* y,
                         size_t y_len, double* z, size_t z_len, qrmc_srmc_stats_t* stats, char* err,
                         size_t err_len);
@@ -83,6 +83,32 @@ int32_t qrmc_srmc_solve(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_
 int32_t qrmc_srmc_evaluate(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg,
                            const double* y_step, const double* x, int64_t npts, double* out,
                            char* err, size_t err_len);
+
+/* ---- plans: the backward solve with device-resident tables, sharded over ranks ----
+ * Hypercubes are partitioned over the ranks (north_star item 5): rank r of `world` owns
+ * the cells [r*c, min((r+1)*c, cells)), c = ceil(cells / world) (qrmc_srmc_cell_range),
+ * computes only those each backward step, and the step's y table is all-gathered over
+ * NCCL (in place, NVLink) before the next step, because endpoints land in arbitrary
+ * cells. Z (read only inside its own cell) is gathered once at the end when kept. Every
+ * cell depends only on (seed, step, cell) and the gathered table, so the tables are
+ * bitwise identical for every world size. world == 1: nccl_unique_id may be NULL. A
+ * non-finite coefficient in any rank's rows of any step fails every rank with
+ * QRMC_ENUMERIC. The plan owns its device tables (allocated once, reused by every run). */
+typedef struct qrmc_srmc_plan qrmc_srmc_plan_t;
+/* 128 bytes: an NCCL unique id made on rank 0, broadcast by the caller */
+int32_t qrmc_srmc_nccl_unique_id(void* out128, char* err, size_t err_len);
+int32_t qrmc_srmc_plan_create(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, int32_t device,
+                              int32_t rank, int32_t world, const void* nccl_unique_id, int32_t keep_z,
+                              qrmc_srmc_plan_t** out, char* err, size_t err_len);
+/* the whole backward loop on the device (one launch + one all-gather per step) */
+int32_t qrmc_srmc_plan_run(qrmc_srmc_plan_t* plan, qrmc_srmc_stats_t* stats, char* err, size_t err_len);
+/* all cells' tables to the host (y: steps * cells * P; z: steps * cells * d * P or NULL) */
+int32_t qrmc_srmc_plan_download(qrmc_srmc_plan_t* plan, double* y, size_t y_len, double* z, size_t z_len,
+                                char* err, size_t err_len);
+void* qrmc_srmc_plan_stream(const qrmc_srmc_plan_t* plan); /* the cudaStream_t every launch uses */
+void qrmc_srmc_plan_destroy(qrmc_srmc_plan_t* plan);
+/* rank's cells [*k0, *k1) (host-only) */
+int32_t qrmc_srmc_cell_range(int64_t cells, int32_t rank, int32_t world, int64_t* k0, int64_t* k1);
 
 /* One backward step on DEVICE tables for the cells [k_begin, k_end) on `stream`
  * (cudaStream_t, NULL = legacy default): next_dev = step-(step+1) y table (unused at the

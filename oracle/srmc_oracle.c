@@ -23,7 +23,7 @@ typedef struct {
     int kind, d, n, P, last;
     int64_t cells, M;
     uint64_t seed;
-    double lo, hi, h, inv2h, dt, sqrt_dt, t, T, L, bdt, sig;
+    double lo, hi, h, inv_h, inv2h, dt, inv_dt, sqrt_dt, t, T, L, bdt, sig, theta, inv_sig;
     double p[8];
 } srmc_t;
 
@@ -31,7 +31,7 @@ static double s_terminal(const srmc_t* s, const double* x) {
     double sum = 0.0;
     for (int l = 0; l < s->d; ++l) sum += x[l];
     if (s->kind == QRMC_SRMC_SIN_BENCH) return (1.0 + s->p[0]) + sin(s->p[1] * sum);
-    const double v = exp(sum / (double)s->d) - s->p[4];
+    const double v = exp(sum * (1.0 / (double)s->d)) - s->p[4]; /* the reciprocal, as the device */
     return v > 0.0 ? v : 0.0;
 }
 
@@ -45,12 +45,11 @@ static double s_driver(const srmc_t* s, const double* x, double y, const double*
         const double ww = w * w;
         return ww < 1.0 ? ww : 1.0;
     }
-    const double mu = s->p[0], sg = s->p[1], rl = s->p[2], rb = s->p[3];
+    const double rl = s->p[2], rb = s->p[3];
     double zs = 0.0;
     for (int l = 0; l < s->d; ++l) zs += z[l];
-    const double theta = (mu - rl) / sg;
-    const double borrow = zs / sg - y;
-    return ((-rl) * y - theta * zs) + (rb - rl) * (borrow > 0.0 ? borrow : 0.0);
+    const double borrow = zs * s->inv_sig - y;
+    return ((-rl) * y - s->theta * zs) + (rb - rl) * (borrow > 0.0 ? borrow : 0.0);
 }
 
 static double s_eval(const srmc_t* s, const double* tab, const double* x) {
@@ -59,7 +58,7 @@ static double s_eval(const srmc_t* s, const double* tab, const double* x) {
     for (int l = 0; l < s->d; ++l) {
         double xc = x[l] < s->lo ? s->lo : x[l];
         xc = xc > s->hi ? s->hi : xc;
-        int c = (int)floor((xc - s->lo) / s->h);
+        int c = (int)floor((xc - s->lo) * s->inv_h); /* reciprocal of h, as the device */
         c = c < 0 ? 0 : (c >= s->n ? s->n - 1 : c);
         k = k * s->n + c;
         const double centre = s->lo + ((double)c + 0.5) * s->h;
@@ -143,7 +142,7 @@ static void s_cell(const srmc_t* s, int step, const double* next, int64_t k, int
             for (int b = 0; b < P; ++b) A[a * P + b] += phi[a] * phi[b];
         if (anyz)
             for (int l = 0; l < d; ++l) {
-                const double rz = (y1 * dw[l]) / s->dt;
+                const double rz = (y1 * dw[l]) * s->inv_dt;
                 for (int p = 0; p < P; ++p) bz[l * P + p] += rz * phi[p];
             }
         if (!zpass) {
@@ -184,13 +183,17 @@ static void s_init(srmc_t* s, const qrmc_srmc_problem_t* prob, const qrmc_srmc_c
     s->lo = cfg->lo;
     s->hi = cfg->hi;
     s->h = (cfg->hi - cfg->lo) / cfg->cells_per_dim;
+    s->inv_h = 1.0 / s->h;
     s->inv2h = 2.0 / s->h;
     s->T = prob->horizon;
     s->dt = prob->horizon / cfg->steps;
+    s->inv_dt = 1.0 / s->dt;
     s->sqrt_dt = sqrt(s->dt);
     s->L = cfg->truncation;
     for (int j = 0; j < 8; ++j) s->p[j] = prob->params[j];
     if (s->kind == QRMC_SRMC_BERGMAN) {
+        s->theta = (prob->params[0] - prob->params[2]) / prob->params[1];
+        s->inv_sig = 1.0 / prob->params[1];
         const double drift = prob->params[0] - 0.5 * (prob->params[1] * prob->params[1]);
         s->bdt = drift * s->dt;
         s->sig = prob->params[1];
@@ -240,6 +243,7 @@ double srmc_oracle_eval(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_
     s.lo = cfg->lo;
     s.hi = cfg->hi;
     s.h = (cfg->hi - cfg->lo) / cfg->cells_per_dim;
+    s.inv_h = 1.0 / s.h;
     s.inv2h = 2.0 / s.h;
     return s_eval(&s, y_step, x);
 }

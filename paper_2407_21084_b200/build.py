@@ -55,8 +55,8 @@ def needs_build() -> bool:
 
 
 SRMC_OUT = PKG / "_lib" / "libqrmc_srmc.so"
-SRMC_SOURCES = [CSRC / "srmc.cu"]
-SRMC_HEADERS = [CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", ROOT / "include" / "qrmc_srmc.h",
+SRMC_SOURCES = [CSRC / "srmc.cu", CSRC / "srmc_host.cpp"]
+SRMC_HEADERS = [CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "srmc_types.h", ROOT / "include" / "qrmc_srmc.h",
                 ROOT / "include" / "qrmc_gpu.h", ROOT / "include" / "qrmc_normal_quantile.h"]
 
 
@@ -70,7 +70,7 @@ def build_srmc(force: bool = False, verbose: bool = False) -> Path:
     tmp = SRMC_OUT.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-shared", "-Xcompiler",
            "-fPIC", "-Xptxas", "-warn-spills", f"-I{ROOT / 'include'}", f"-I{CSRC}", *map(str, SRMC_SOURCES), "-o",
-           str(tmp)]
+           str(tmp), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

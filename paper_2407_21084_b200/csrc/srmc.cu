@@ -26,22 +26,13 @@
 
 #include "qrmc_device.cuh"
 #include "qrmc_srmc.h"
+#include "srmc_types.h"
 
-namespace {
+namespace qrmc_srmc_dev {
 
 using namespace qrmc_dev;
 
-struct SrmcDev {
-    int kind, n, step, last;
-    int64_t cells, M;
-    int64_t k0, k1;  // this launch's cell range [k0, k1) (a rank's shard; [0, cells) single-GPU)
-    uint64_t seed;
-    double lo, hi, h, inv2h, dt, sqrt_dt, t, T, L;
-    double p[8];
-    double bdt, sig;  // Euler: x + bdt + sig * sqrt_dt * z
-    uint32_t rk[20];  // Philox round keys (seed + r * Weyl), read from the constant bank
-    double decay;     // SinBenchmark exp(lambda^2 d (t - T) / 2) at this step's t (hoisted per launch)
-};
+namespace {
 
 template <int D>
 __device__ __forceinline__ double srmc_terminal(const SrmcDev& s, const double* x) {
@@ -49,7 +40,7 @@ __device__ __forceinline__ double srmc_terminal(const SrmcDev& s, const double* 
 #pragma unroll
     for (int l = 0; l < D; ++l) sum = DADD(sum, x[l]);
     if (s.kind == QRMC_SRMC_SIN_BENCH) return DADD(DADD(1.0, s.p[0]), sin(DMUL(s.p[1], sum)));
-    const double v = DSUB(exp(DDIV(sum, static_cast<double>(D))), s.p[4]);
+    const double v = DSUB(exp(DMUL(sum, 1.0 / D)), s.p[4]);  // 1/D: a compile-time constant, as the oracle's
     return v > 0.0 ? v : 0.0;
 }
 
@@ -64,12 +55,12 @@ __device__ __forceinline__ double srmc_driver(const SrmcDev& s, const double* x,
         const double ww = DMUL(w, w);
         return ww < 1.0 ? ww : 1.0;
     }
-    const double mu = s.p[0], sg = s.p[1], rl = s.p[2], rb = s.p[3];
+    // p[5] = theta = (mu - r_l) / sigma and p[6] = 1 / sigma, hoisted to the host (make_dev)
+    const double rl = s.p[2], rb = s.p[3], theta = s.p[5], inv_sg = s.p[6];
     double zs = 0.0;
 #pragma unroll
     for (int l = 0; l < D; ++l) zs = DADD(zs, z[l]);
-    const double theta = DDIV(DSUB(mu, rl), sg);
-    const double borrow = DSUB(DDIV(zs, sg), y);
+    const double borrow = DSUB(DMUL(zs, inv_sg), y);
     return DADD(DSUB(DMUL(-rl, y), DMUL(theta, zs)), DMUL(DSUB(rb, rl), borrow > 0.0 ? borrow : 0.0));
 }
 
@@ -82,7 +73,7 @@ __device__ __forceinline__ double srmc_eval(const SrmcDev& s, const double* __re
     for (int l = 0; l < D; ++l) {
         double xc = x[l] < s.lo ? s.lo : x[l];
         xc = xc > s.hi ? s.hi : xc;
-        int c = static_cast<int>(floor(DDIV(DSUB(xc, s.lo), s.h)));
+        int c = static_cast<int>(floor(DMUL(DSUB(xc, s.lo), s.inv_h)));  // the reciprocal, as the oracle
         c = c < 0 ? 0 : (c >= s.n ? s.n - 1 : c);
         k = k * s.n + c;
         const double centre = DADD(s.lo, DMUL(DADD(static_cast<double>(c), 0.5), s.h));
@@ -268,7 +259,7 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
         if constexpr (ANYZ) {
 #pragma unroll
             for (int l = 0; l < D; ++l) {
-                const double rz = DDIV(DMUL(y1, dw[l]), s.dt);
+                const double rz = DMUL(DMUL(y1, dw[l]), s.inv_dt);
 #pragma unroll
                 for (int p = 0; p < P; ++p) bz[l * P + p] += rz * phi[p];
             }
@@ -304,8 +295,13 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
     warp_sum<P, G>(by);
     chol_solve<P, 1>(A, by);
     if (live && sub == 0) {
+        bool finite = true;
 #pragma unroll
-        for (int p = 0; p < P; ++p) ytab[k * P + p] = by[p];
+        for (int p = 0; p < P; ++p) {
+            ytab[k * P + p] = by[p];
+            finite = finite && isfinite(by[p]);
+        }
+        if (!finite) *s.bad = 1;  // NumericError (every step's table, not only the last)
         if constexpr (ANYZ) {
 #pragma unroll
             for (int j = 0; j < D * P; ++j) ztab[k * D * P + j] = bz[j];
@@ -323,6 +319,8 @@ __global__ void k_srmc_eval(SrmcDev s, const double* __restrict__ tab, const dou
     for (int l = 0; l < D; ++l) xi[l] = x[i * D + l];
     out[i] = srmc_eval<D, P>(s, tab, xi);
 }
+
+}  // namespace
 
 void set_err(char* err, size_t len, const char* msg) {
     if (err && len) {
@@ -372,13 +370,17 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
     s.lo = c->lo;
     s.hi = c->hi;
     s.h = (c->hi - c->lo) / c->cells_per_dim;
+    s.inv_h = 1.0 / s.h;
     s.inv2h = 2.0 / s.h;
     s.T = p->horizon;
     s.dt = p->horizon / c->steps;
+    s.inv_dt = 1.0 / s.dt;
     s.sqrt_dt = std::sqrt(s.dt);
     s.L = c->truncation;
     for (int j = 0; j < 8; ++j) s.p[j] = p->params[j];
     if (p->kind == QRMC_SRMC_BERGMAN) {
+        s.p[5] = (p->params[0] - p->params[2]) / p->params[1];  // theta
+        s.p[6] = 1.0 / p->params[1];
         volatile double drift = p->params[0] - 0.5 * (p->params[1] * p->params[1]);
         s.bdt = drift * s.dt;
         s.sig = p->params[1];
@@ -390,7 +392,7 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
 }
 
 template <int D, int P>
-void launch_step(const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz, cudaStream_t st) {
+void launch_step_t(const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz, cudaStream_t st) {
     const int warps = 8;
     const int64_t cells = s.k1 - s.k0;
     // 8 lanes per hypercube, 4 hypercubes per warp -- only when the range still fills the
@@ -420,13 +422,13 @@ template <int D>
 void launch_step_d(int P, const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz,
                    cudaStream_t st) {
     if (P == 1)
-        launch_step<D, 1>(s, next, y, z, zpass, wantz, st);
+        launch_step_t<D, 1>(s, next, y, z, zpass, wantz, st);
     else
-        launch_step<D, D + 1>(s, next, y, z, zpass, wantz, st);
+        launch_step_t<D, D + 1>(s, next, y, z, zpass, wantz, st);
 }
 
-void dispatch_step(int d, int P, const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz,
-                   cudaStream_t st) {
+cudaError_t launch_step(int d, int P, const SrmcDev& s, const double* next, double* y, double* z, bool zpass,
+                        bool wantz, cudaStream_t st) {
     switch (d) {
         case 1: launch_step_d<1>(P, s, next, y, z, zpass, wantz, st); break;
         case 2: launch_step_d<2>(P, s, next, y, z, zpass, wantz, st); break;
@@ -435,6 +437,7 @@ void dispatch_step(int d, int P, const SrmcDev& s, const double* next, double* y
         case 5: launch_step_d<5>(P, s, next, y, z, zpass, wantz, st); break;
         default: launch_step_d<6>(P, s, next, y, z, zpass, wantz, st); break;
     }
+    return cudaGetLastError();
 }
 
 template <int D>
@@ -456,7 +459,9 @@ void launch_eval_d(int P, const SrmcDev& s, const double* tab, const double* x, 
         }                                                                         \
     } while (0)
 
-}  // namespace
+}  // namespace qrmc_srmc_dev
+
+using namespace qrmc_srmc_dev;
 
 extern "C" int32_t qrmc_srmc_basis_size(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg) {
     if (validate(prob, cfg, nullptr, 0) != QRMC_OK) return -1;
@@ -468,71 +473,6 @@ extern "C" int64_t qrmc_srmc_cells(const qrmc_srmc_problem_t* prob, const qrmc_s
     int64_t c = 1;
     for (int l = 0; l < prob->dim; ++l) c *= cfg->cells_per_dim;
     return c;
-}
-
-extern "C" int32_t qrmc_srmc_solve(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg, double* y,
-                                   size_t y_len, double* z, size_t z_len, qrmc_srmc_stats_t* stats, char* err,
-                                   size_t err_len) {
-    char msg[256] = {0};
-    int rc = validate(prob, cfg, err, err_len);
-    if (rc != QRMC_OK) return rc;
-    const int d = prob->dim;
-    const int P = cfg->basis == QRMC_SRMC_LP1 ? d + 1 : 1;
-    SrmcDev s = make_dev(prob, cfg);
-    const bool zpass = needs_z(prob);
-    const bool wantz = !zpass && cfg->want_z != 0;
-    const size_t per_y = static_cast<size_t>(s.cells) * P;
-    const size_t per_z = per_y * d;
-    const int N = cfg->steps;
-    if (!y || y_len < per_y * N) return set_err(err, err_len, "y buffer too small (steps * cells * P)"), QRMC_EINVAL;
-    const bool outz = z != nullptr;
-    if (outz && z_len < per_z * N) return set_err(err, err_len, "z buffer too small (steps * cells * d * P)"), QRMC_EINVAL;
-    double *dy = nullptr, *dz = nullptr;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    cudaStream_t st = nullptr;
-    const bool anyz = zpass || wantz || outz;
-    float ms = 0.f;
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaMalloc(&dy, per_y * N * sizeof(double)));
-    if (anyz) CK(cudaMalloc(&dz, per_z * N * sizeof(double)));
-    CK(cudaEventRecord(e0, st));
-    for (int i = N - 1; i >= 0; --i) {
-        s.step = i;
-        s.last = (i == N - 1);
-        s.t = (i + 1) * s.dt;  // the driver is evaluated at (t_{i+1}, X_{i+1}, Y1, Zhat_i(X_i))
-        s.decay = std::exp(((s.p[1] * s.p[1]) * static_cast<double>(d)) * (s.t - s.T) / 2.0);
-        dispatch_step(d, P, s, s.last ? nullptr : dy + per_y * (i + 1), dy + per_y * i, anyz ? dz + per_z * i : nullptr,
-                      zpass, !zpass && (wantz || outz), st);
-        CK(cudaGetLastError());
-    }
-    CK(cudaEventRecord(e1, st));
-    CK(cudaEventSynchronize(e1));
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    CK(cudaMemcpyAsync(y, dy, per_y * N * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (outz) CK(cudaMemcpyAsync(z, dz, per_z * N * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (size_t j = 0; j < per_y; ++j)
-        if (!std::isfinite(y[j])) {
-            std::snprintf(msg, sizeof msg, "non-finite coefficient at step 0");
-            rc = QRMC_ENUMERIC;
-            goto done;
-        }
-    if (stats) {
-        stats->path_steps = static_cast<uint64_t>(s.cells) * static_cast<uint64_t>(s.M) * N;
-        stats->path_passes = zpass ? 2 : 1;
-        stats->device_seconds = ms * 1e-3;
-        stats->kernel_launches = N;
-    }
-done:
-    if (dy) cudaFree(dy);
-    if (dz) cudaFree(dz);
-    if (e0) cudaEventDestroy(e0);
-    if (e1) cudaEventDestroy(e1);
-    if (st) cudaStreamDestroy(st);
-    if (rc != QRMC_OK) set_err(err, err_len, msg);
-    return rc;
 }
 
 extern "C" int32_t qrmc_srmc_evaluate(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_t* cfg,
@@ -570,6 +510,16 @@ done:
     return rc;
 }
 
+// qrmc_srmc_step_device has no plan to report through: its non-finite flag goes to a
+// per-device scratch word (the plan of srmc_host.cpp checks its own).
+static int* bad_scratch() {
+    static int* p[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!p[dev & 63]) cudaMalloc(&p[dev & 63], sizeof(int));
+    return p[dev & 63];
+}
+
 // One backward step on caller-owned device tables for the cell range [k_begin, k_end):
 // the sharded (multi-GPU) driver runs it on its own cells, then all-gathers the step's
 // table (paper_2407_21084_b200/srmc.py, solve_sharded). Results per cell do not depend
@@ -594,9 +544,9 @@ extern "C" int32_t qrmc_srmc_step_device(const qrmc_srmc_problem_t* prob, const 
     s.last = (step == cfg->steps - 1);
     s.t = (step + 1) * s.dt;
     s.decay = std::exp(((s.p[1] * s.p[1]) * static_cast<double>(d)) * (s.t - s.T) / 2.0);
-    dispatch_step(d, P, s, s.last ? nullptr : next_dev, y_dev, z_dev, zpass, !zpass && z_dev != nullptr,
-                  static_cast<cudaStream_t>(stream));
-    CK(cudaGetLastError());
+    s.bad = bad_scratch();
+    CK(launch_step(d, P, s, s.last ? nullptr : next_dev, y_dev, z_dev, zpass, !zpass && z_dev != nullptr,
+                   static_cast<cudaStream_t>(stream)));
 done:
     if (rc != QRMC_OK) set_err(err, err_len, msg);
     return rc;

@@ -66,6 +66,22 @@ def lib() -> C.CDLL:
         L.qrmc_srmc_solve.restype = C.c_int32
         L.qrmc_srmc_evaluate.argtypes = [P, Cf, dp, dp, C.c_int64, dp, C.c_char_p, C.c_size_t]
         L.qrmc_srmc_evaluate.restype = C.c_int32
+        vp = C.c_void_p
+        L.qrmc_srmc_nccl_unique_id.argtypes = [vp, C.c_char_p, C.c_size_t]
+        L.qrmc_srmc_nccl_unique_id.restype = C.c_int32
+        L.qrmc_srmc_plan_create.argtypes = [P, Cf, C.c_int32, C.c_int32, C.c_int32, vp, C.c_int32, C.POINTER(vp),
+                                            C.c_char_p, C.c_size_t]
+        L.qrmc_srmc_plan_create.restype = C.c_int32
+        L.qrmc_srmc_plan_run.argtypes = [vp, C.POINTER(SrmcStats), C.c_char_p, C.c_size_t]
+        L.qrmc_srmc_plan_run.restype = C.c_int32
+        L.qrmc_srmc_plan_download.argtypes = [vp, dp, C.c_size_t, dp, C.c_size_t, C.c_char_p, C.c_size_t]
+        L.qrmc_srmc_plan_download.restype = C.c_int32
+        L.qrmc_srmc_plan_stream.argtypes = [vp]
+        L.qrmc_srmc_plan_stream.restype = vp
+        L.qrmc_srmc_plan_destroy.argtypes = [vp]
+        L.qrmc_srmc_plan_destroy.restype = None
+        L.qrmc_srmc_cell_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.qrmc_srmc_cell_range.restype = C.c_int32
         _LIB = L
     return _LIB
 
@@ -159,6 +175,80 @@ def solve(problem: SrmcProblem, cfg: SrmcConfig, with_z: bool = False) -> SrmcTa
                                           "kernel_launches": st.kernel_launches, "path_passes": st.path_passes})
 
 
+class SrmcPlan:
+    """qrmc_srmc_plan_* (include/qrmc_srmc.h): device-resident tables, the backward loop
+    over this rank's hypercubes with an NCCL all-gather of every step's table when
+    world > 1 (the library's own communicator; `nccl_id` comes from rank 0's
+    ``nccl_unique_id()``, broadcast by the caller)."""
+
+    def __init__(self, problem: SrmcProblem, cfg: SrmcConfig, device: int = 0, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None, keep_z: bool = False):
+        L = lib()
+        self.problem, self.config, self.world, self.rank = problem, cfg, world, rank
+        self.handle = C.c_void_p()
+        err = C.create_string_buffer(512)
+        uid = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        rc = L.qrmc_srmc_plan_create(C.byref(problem), C.byref(cfg), device, rank, world,
+                                     C.cast(uid, C.c_void_p) if uid is not None else None, int(keep_z),
+                                     C.byref(self.handle), err, 512)
+        if rc:
+            raise SrmcError(rc, err.value.decode())
+        self.keep_z = keep_z
+
+    def run(self) -> dict:
+        st = SrmcStats()
+        err = C.create_string_buffer(512)
+        rc = lib().qrmc_srmc_plan_run(self.handle, C.byref(st), err, 512)
+        if rc:
+            raise SrmcError(rc, err.value.decode())
+        return {"path_steps": st.path_steps, "device_seconds": st.device_seconds,
+                "kernel_launches": st.kernel_launches, "path_passes": st.path_passes}
+
+    def download(self, with_z: bool = False) -> SrmcTables:
+        p, c = self.problem, self.config
+        P = p.dim + 1 if c.basis == LP1 else 1
+        cells = c.cells_per_dim ** p.dim
+        y = np.empty((c.steps, cells, P))
+        z = np.empty((c.steps, cells, p.dim, P)) if with_z else None
+        dp = C.POINTER(C.c_double)
+        err = C.create_string_buffer(512)
+        rc = lib().qrmc_srmc_plan_download(self.handle, y.ctypes.data_as(dp), y.size,
+                                           z.ctypes.data_as(dp) if z is not None else None,
+                                           z.size if z is not None else 0, err, 512)
+        if rc:
+            raise SrmcError(rc, err.value.decode())
+        return SrmcTables(p, c, y, z)
+
+    def stream(self) -> int:
+        return lib().qrmc_srmc_plan_stream(self.handle)
+
+    def close(self) -> None:
+        if self.handle:
+            lib().qrmc_srmc_plan_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    err = C.create_string_buffer(256)
+    rc = lib().qrmc_srmc_nccl_unique_id(buf, err, 256)
+    if rc:
+        raise SrmcError(rc, err.value.decode())
+    return bytes(buf)
+
+
+def cell_range(cells: int, rank: int, world: int) -> tuple[int, int]:
+    k0, k1 = C.c_int64(), C.c_int64()
+    assert lib().qrmc_srmc_cell_range(cells, rank, world, C.byref(k0), C.byref(k1)) == 0
+    return k0.value, k1.value
+
+
 def _device_step_fn(problem: SrmcProblem, cfg: SrmcConfig):
     """step_fn for solve_sharded: qrmc_srmc_step_device on the current CUDA stream."""
     import torch
@@ -192,6 +282,23 @@ def solve_sharded(problem: SrmcProblem, cfg: SrmcConfig, with_z: bool = False, g
     import torch.distributed as dist
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if step_fn is None and (world == 1 or dist.get_backend(group) == "nccl"):
+        # the library's plan: its own NCCL communicator all-gathers every step's table
+        nid = None
+        if world > 1:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            nid = obj[0]
+        plan = SrmcPlan(problem, cfg, torch.cuda.current_device(), rank, world, nid, keep_z=with_z)
+        try:
+            st = plan.run()
+            t = plan.download(with_z)
+        finally:
+            plan.close()
+        k0, k1 = cell_range(cfg.cells_per_dim ** problem.dim, rank, world)
+        t.stats = dict(st, cells=(k0, k1))
+        return t
     d = problem.dim
     P = d + 1 if cfg.basis == LP1 else 1
     cells = cfg.cells_per_dim ** d

@@ -42,7 +42,9 @@ def test_library_exports_and_host_validation():
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     declared = set(re.findall(r"\b(qrmc_srmc_\w+)\s*\(", text))
     assert declared == {"qrmc_srmc_basis_size", "qrmc_srmc_cells", "qrmc_srmc_solve", "qrmc_srmc_evaluate",
-                        "qrmc_srmc_step_device"}
+                        "qrmc_srmc_step_device", "qrmc_srmc_nccl_unique_id", "qrmc_srmc_plan_create",
+                        "qrmc_srmc_plan_run", "qrmc_srmc_plan_download", "qrmc_srmc_plan_stream",
+                        "qrmc_srmc_plan_destroy", "qrmc_srmc_cell_range"}
     for sym in declared:
         assert hasattr(L, sym), sym
     p = srmc.sin_bench_problem(3)
@@ -53,6 +55,27 @@ def test_library_exports_and_host_validation():
     assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(c0)) == 1
     bad = srmc.config(4, 5, 3, basis=srmc.LP1)  # M < P
     assert L.qrmc_srmc_basis_size(C.byref(p), C.byref(bad)) == -1
+
+
+def test_cell_range_partitions_the_hypercubes():
+    for cells in (1, 7, 64, 4096, 16 ** 6):
+        for world in (1, 2, 3, 4, 8):
+            ranges = [srmc.cell_range(cells, r, world) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == cells
+            assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+            assert max(k1 - k0 for k0, k1 in ranges) - min(k1 - k0 for k0, k1 in ranges) <= -(-cells // world)
+
+
+def test_plan_rejects_bad_input_before_touching_the_device():
+    p = srmc.sin_bench_problem(2)
+    with pytest.raises(srmc.SrmcError) as e:
+        srmc.SrmcPlan(p, srmc.config(0, 4, 64))
+    assert e.value.code == 1
+    with pytest.raises(srmc.SrmcError) as e:
+        srmc.SrmcPlan(p, srmc.config(3, 4, 64), rank=1, world=2)  # world > 1 without an NCCL id
+    assert e.value.code == 1 and "NCCL" in str(e.value)
+    with pytest.raises(srmc.SrmcError):
+        srmc.SrmcPlan(p, srmc.config(1 << 22, 4, 64))  # stream-id layout (rng.hpp:73-80)
 
 
 def test_srmc_library_is_sm100a():
@@ -223,3 +246,31 @@ def test_gpu_per_range_steps_are_bitwise_equal_to_the_whole_solve(name, mk, kw):
     assert np.array_equal(z.cpu().numpy(), whole.z)
     g1 = srmc.solve_sharded(p, c, with_z=True)
     assert np.array_equal(g1.y, whole.y) and np.array_equal(g1.z, whole.z)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,mk,kw", [PARITY_CASES[i] for i in (1, 3, 8)], ids=[PARITY_CASES[i][0] for i in (1, 3, 8)])
+def test_plan_runs_repeatably_and_equals_the_one_shot_solve(name, mk, kw):
+    """qrmc_srmc_plan_*: the tables stay on the device across runs (allocated once) and
+    every run reproduces qrmc_srmc_solve bit for bit."""
+    p = mk()
+    c = srmc.config(seed=7, **kw)
+    whole = srmc.solve(p, c, with_z=True)
+    plan = srmc.SrmcPlan(p, c, keep_z=True)
+    try:
+        for _ in range(2):
+            st = plan.run()
+            t = plan.download(with_z=True)
+            assert np.array_equal(t.y, whole.y) and np.array_equal(t.z, whole.z)
+            assert st["path_steps"] == c.cells_per_dim ** p.dim * c.paths_per_cell * c.steps
+    finally:
+        plan.close()
+
+
+@pytest.mark.gpu
+def test_plan_reports_non_finite_tables():
+    p = srmc.sin_bench_problem(2)
+    p.params[1] = float("nan")  # lambda = NaN: every coefficient non-finite
+    with pytest.raises(srmc.SrmcError) as e:
+        srmc.solve(p, srmc.config(3, 4, 64))
+    assert e.value.code == 2
