@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define QRMC_GPU_ABI_VERSION 1
+#define QRMC_GPU_ABI_VERSION 2
 
 typedef enum qrmc_status {
     QRMC_OK = 0,
@@ -75,12 +75,15 @@ enum {
                                  p = {kappa, lambda}                (benchmark.cpp:55-62) */
 };
 enum {
-    QRMC_DRIFT_ZERO = 0, /* null drift (sde.hpp:23) */
-    QRMC_DRIFT_CONST = 1 /* b_l = c, p = {c}; fault injection as in test_sde.cpp:143-158 */
+    QRMC_DRIFT_ZERO = 0,  /* null drift (sde.hpp:23) */
+    QRMC_DRIFT_CONST = 1, /* b_l = c, p = {c}; fault injection as in test_sde.cpp:143-158 */
+    QRMC_DRIFT_AFFINE = 2 /* b_l(t, x) = drift_vec[l] + drift_vec[8 + l] * x_l (per-coordinate,
+                             e.g. Ornstein-Uhlenbeck), evaluated at the pre-step state (sde.cpp:54-60) */
 };
 enum {
     QRMC_DIFFUSION_IDENTITY = 0, /* null diffusion_apply: out = dw (sde.cpp:48-53) */
-    QRMC_DIFFUSION_SCALAR = 1    /* out = sigma * dw, p = {sigma}, requires brownian_dim == dim */
+    QRMC_DIFFUSION_SCALAR = 1,   /* out = sigma * dw, p = {sigma}, requires brownian_dim == dim */
+    QRMC_DIFFUSION_DIAG = 2      /* out_l = diffusion_vec[l] * dw_l, requires brownian_dim == dim */
 };
 
 typedef struct qrmc_problem {
@@ -99,6 +102,9 @@ typedef struct qrmc_problem {
     double growth_g, growth_exp_g, growth_f, growth_exp_f, lipschitz_f;
     double moment_ratio; /* C_eta >= 1 */
     double state_bound;  /* |X| beyond this aborts with QRMC_ESIM */
+    /* per-coordinate functor data (ABI version 2): QRMC_DRIFT_AFFINE, QRMC_DIFFUSION_DIAG */
+    double drift_vec[16];
+    double diffusion_vec[8];
 } qrmc_problem_t;
 
 typedef struct qrmc_config {

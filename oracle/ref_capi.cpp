@@ -146,6 +146,11 @@ ProblemSpec to_spec(const qrmc_problem_t& p) {
         spec.drift = [c](double, std::span<const double>, std::span<double> out) {
             for (double& v : out) v = c;
         };
+    } else if (p.drift_kind == QRMC_DRIFT_AFFINE) {
+        std::vector<double> a(p.drift_vec, p.drift_vec + 8), b(p.drift_vec + 8, p.drift_vec + 16);
+        spec.drift = [a, b](double, std::span<const double> x, std::span<double> out) {
+            for (std::size_t l = 0; l < out.size(); ++l) out[l] = a[l] + b[l] * x[l];
+        };
     } else if (p.drift_kind != QRMC_DRIFT_ZERO) {
         throw std::invalid_argument("unknown drift kind");
     }
@@ -154,6 +159,12 @@ ProblemSpec to_spec(const qrmc_problem_t& p) {
         spec.diffusion_apply = [s](double, std::span<const double>, std::span<const double> dw,
                                    std::span<double> out) {
             for (std::size_t l = 0; l < out.size(); ++l) out[l] = s * dw[l];
+        };
+    } else if (p.diffusion_kind == QRMC_DIFFUSION_DIAG) {
+        std::vector<double> sg(p.diffusion_vec, p.diffusion_vec + 8);
+        spec.diffusion_apply = [sg](double, std::span<const double>, std::span<const double> dw,
+                                    std::span<double> out) {
+            for (std::size_t l = 0; l < out.size(); ++l) out[l] = sg[l] * dw[l];
         };
     } else if (p.diffusion_kind != QRMC_DIFFUSION_IDENTITY) {
         throw std::invalid_argument("unknown diffusion kind");

@@ -1,9 +1,11 @@
-// Boost.Math students_t stand-in (oracle build only). The reference reaches it
-// only for Student measures with mu not in {1, 2} (proj/src/student.cpp:60,73),
-// which no configuration on the hot path uses. The
-// stub throws so an out-of-scope use is loud, never silently wrong.
+// Boost.Math students_t stand-in (oracle build only). The reference reaches it only for
+// Student measures with mu not in {1, 2} (proj/src/student.cpp:60, 73). Boost is not
+// vendored and its version is unpinned, so the CDF and quantile are DEFINED by
+// include/qrmc_student_t.h (regularised incomplete beta by continued fraction, safeguarded
+// Newton for the quantile) -- the same definition the C restatement and the device use.
+// Parity with real Boost is unpinned.
 #pragma once
-#include <stdexcept>
+#include "qrmc_student_t.h"
 namespace boost {
 namespace math {
 template <class T>
@@ -12,12 +14,12 @@ struct students_t_distribution {
     T df_;
 };
 template <class T>
-inline T cdf(const students_t_distribution<T>&, T) {
-    throw std::domain_error("oracle shim: general-mu Student measure is out of scope");
+inline T cdf(const students_t_distribution<T>& d, T t) {
+    return qrmc_student_cdf(t, d.df_);
 }
 template <class T>
-inline T quantile(const students_t_distribution<T>&, T) {
-    throw std::domain_error("oracle shim: general-mu Student measure is out of scope");
+inline T quantile(const students_t_distribution<T>& d, T u) {
+    return qrmc_student_quantile(u, d.df_);
 }
 }  // namespace math
 }  // namespace boost

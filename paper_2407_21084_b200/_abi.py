@@ -26,8 +26,8 @@ GAMMA_KINDS = {"full": GAMMA_FULL, "total": GAMMA_TOTAL, "hyperbolic": GAMMA_HYP
 MEMORY_STORE, MEMORY_RECOMPUTE = 0, 1
 TERMINAL_SIN_SUM, TERMINAL_CONST, TERMINAL_X0, TERMINAL_NAN = 0, 1, 2, 3
 DRIVER_ZERO, DRIVER_CONST, DRIVER_Y, DRIVER_SIN_BENCH = 0, 1, 2, 3
-DRIFT_ZERO, DRIFT_CONST = 0, 1
-DIFFUSION_IDENTITY, DIFFUSION_SCALAR = 0, 1
+DRIFT_ZERO, DRIFT_CONST, DRIFT_AFFINE = 0, 1, 2
+DIFFUSION_IDENTITY, DIFFUSION_SCALAR, DIFFUSION_DIAG = 0, 1, 2
 
 
 class Problem(C.Structure):
@@ -42,6 +42,7 @@ class Problem(C.Structure):
         ("growth_g", C.c_double), ("growth_exp_g", C.c_double), ("growth_f", C.c_double),
         ("growth_exp_f", C.c_double), ("lipschitz_f", C.c_double),
         ("moment_ratio", C.c_double), ("state_bound", C.c_double),
+        ("drift_vec", C.c_double * 16), ("diffusion_vec", C.c_double * 8),
     ]
 
 
@@ -98,7 +99,7 @@ def custom_problem(dim: int, terminal: int, driver: int, *, terminal_params=(), 
                    diffusion_params=(), horizon: float = 1.0, growth_g: float = 0.0,
                    growth_exp_g: float = 0.0, growth_f: float = 0.0, growth_exp_f: float = 0.0,
                    lipschitz_f: float = 0.0, moment_ratio: float = 1.0,
-                   state_bound: float = 1e15) -> Problem:
+                   state_bound: float = 1e15, drift_vec=(), diffusion_vec=()) -> Problem:
     """A ProblemSpec built from device functor kinds (the test problems of
     proj/tests/test_solver.cpp:17-28 and acceptance_main.cpp:228-236)."""
     p = Problem()
@@ -117,6 +118,10 @@ def custom_problem(dim: int, terminal: int, driver: int, *, terminal_params=(), 
         p.drift_params[i] = v
     for i, v in enumerate(diffusion_params):
         p.diffusion_params[i] = v
+    for i, v in enumerate(drift_vec):  # AFFINE: [a_0..a_7, b_0..b_7], b_l(x) = a_l + b_l x_l
+        p.drift_vec[i] = v
+    for i, v in enumerate(diffusion_vec):  # DIAG: sigma_l
+        p.diffusion_vec[i] = v
     p.growth_g, p.growth_exp_g, p.growth_f = growth_g, growth_exp_g, growth_f
     p.growth_exp_f, p.lipschitz_f = growth_exp_f, lipschitz_f
     p.moment_ratio, p.state_bound = moment_ratio, state_bound

@@ -23,7 +23,7 @@ OUT = PKG / "_lib" / "libqrmc_gpu.so"
 SOURCES = [CSRC / "kernels.cu", CSRC / "responses_mma.cu", CSRC / "responses_ws.cu", CSRC / "project_mma.cu", CSRC / "host.cpp",
            CSRC / "table_io.cpp"]
 HEADERS = [CSRC / "kernels.cuh", CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "series_block.cuh", CSRC / "mma_common.cuh", ROOT / "include" / "qrmc_gpu.h",
-           ROOT / "include" / "qrmc_normal_quantile.h"]
+           ROOT / "include" / "qrmc_normal_quantile.h", ROOT / "include" / "qrmc_student_t.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -57,7 +57,8 @@ def needs_build() -> bool:
 SRMC_OUT = PKG / "_lib" / "libqrmc_srmc.so"
 SRMC_SOURCES = [CSRC / "srmc.cu", CSRC / "srmc_host.cpp"]
 SRMC_HEADERS = [CSRC / "qrmc_device.cuh", CSRC / "qrmc_types.h", CSRC / "srmc_types.h", ROOT / "include" / "qrmc_srmc.h",
-                ROOT / "include" / "qrmc_gpu.h", ROOT / "include" / "qrmc_normal_quantile.h"]
+                ROOT / "include" / "qrmc_gpu.h", ROOT / "include" / "qrmc_normal_quantile.h",
+                ROOT / "include" / "qrmc_student_t.h"]
 
 
 def build_srmc(force: bool = False, verbose: bool = False) -> Path:

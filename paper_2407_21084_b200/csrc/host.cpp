@@ -360,9 +360,9 @@ ProblemDev to_device_problem(const qrmc_problem_t& p) {
         fail(QRMC_ENOTIMPL, "terminal kind has no device functor");
     if (p.driver_kind < QRMC_DRIVER_ZERO || p.driver_kind > QRMC_DRIVER_SIN_BENCH)
         fail(QRMC_ENOTIMPL, "driver kind has no device functor");
-    if (p.drift_kind != QRMC_DRIFT_ZERO && p.drift_kind != QRMC_DRIFT_CONST)
+    if (p.drift_kind < QRMC_DRIFT_ZERO || p.drift_kind > QRMC_DRIFT_AFFINE)
         fail(QRMC_ENOTIMPL, "drift kind has no device functor");
-    if (p.diffusion_kind != QRMC_DIFFUSION_IDENTITY && p.diffusion_kind != QRMC_DIFFUSION_SCALAR)
+    if (p.diffusion_kind < QRMC_DIFFUSION_IDENTITY || p.diffusion_kind > QRMC_DIFFUSION_DIAG)
         fail(QRMC_ENOTIMPL, "diffusion kind has no device functor");
     if (p.dim > kMaxDim) fail(QRMC_ENOTIMPL, fmt("dimension %d exceeds the device limit %d", p.dim, kMaxDim));
     if (p.brownian_dim != p.dim)
@@ -381,6 +381,11 @@ ProblemDev to_device_problem(const qrmc_problem_t& p) {
     d.dp1 = p.driver_params[1];
     d.drift_c = p.drift_params[0];
     d.sigma = p.diffusion_params[0];
+    for (int l = 0; l < std::min(p.dim, kMaxDim); ++l) {
+        d.drift_a[l] = p.drift_vec[l];
+        d.drift_b[l] = p.drift_vec[8 + l];
+        d.sig[l] = p.diffusion_vec[l];
+    }
     // lstar_bound's x-independent factor, evaluated exactly as sde.cpp:28-29
     d.lstar_base = p.moment_ratio * (p.growth_g + p.horizon * p.growth_f) *
                    std::exp(p.moment_ratio * p.lipschitz_f * p.horizon);
@@ -400,7 +405,9 @@ MeasureDev to_device_measure(const qrmc_config_t& c, int dim) {
     else if (c.mu == 2.0)
         m.form = 2;
     else
-        fail(QRMC_ENOTIMPL, "general-mu Student measure has no device form (mu must be 1 or 2)");
+        m.form = 3;  // Student's t with mu degrees of freedom (include/qrmc_student_t.h)
+    m.mu = c.mu;
+    m.sqrt_mu = std::sqrt(c.mu);
     for (int l = 0; l < dim; ++l) {
         m.center[l] = c.center ? c.center[l] : 0.0;
         if (!std::isfinite(m.center[l])) fail(QRMC_EINVAL, "SamplingMeasure: center must be finite");

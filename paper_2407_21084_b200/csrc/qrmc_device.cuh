@@ -16,6 +16,7 @@
 
 #include "qrmc_gpu.h"
 #include "qrmc_normal_quantile.h"
+#include "qrmc_student_t.h"
 #include "qrmc_types.h"
 
 namespace qrmc_dev {
@@ -95,6 +96,7 @@ __device__ __forceinline__ uint64_t sid_evaluation(int step, uint64_t point) {
 __device__ __forceinline__ double measure_cdf(const MeasureDev& m, double x, int l) {
     x = DSUB(x, m.center[l]);
     if (m.form == 1) return DADD(0.5, DDIV(atan(x), 3.14159265358979323846));
+    if (m.form == 3) return qrmc_student_cdf(DMUL(x, m.sqrt_mu), m.mu);  // cdf(students_t(mu), x sqrt(mu))
     return DMUL(0.5, DADD(DDIV(x, __dsqrt_rn(DADD(DMUL(x, x), 1.0))), 1.0));
 }
 
@@ -106,6 +108,8 @@ __device__ __forceinline__ double measure_inv_cdf(const MeasureDev& m, double u,
     double c;
     if (m.form == 1)
         c = tan(DMUL(3.14159265358979323846, DSUB(u, 0.5)));
+    else if (m.form == 3)
+        c = DDIV(qrmc_student_quantile(u, m.mu), m.sqrt_mu);  // quantile(students_t(mu), u) / sqrt(mu)
     else
         c = DDIV(DSUB(u, 0.5), __dsqrt_rn(DMUL(u, DSUB(1.0, u))));
     return DADD(c, m.center[l]);
@@ -202,6 +206,19 @@ __device__ __forceinline__ double truncate_soft(double v, double b) {
     return b < v ? b : v;
 }
 
+// One coordinate of euler_step (sde.cpp:37-73): out = sigma(t, x) dw (diffusion_apply,
+// identity when null), x_l += b_l(t, x) dt + out_l with the drift at the pre-step state.
+// Every device drift/diffusion is diagonal, so coordinate l needs only x_l and dw_l.
+__device__ __forceinline__ double euler_coord(const ProblemDev& p, double xo, double dw, int l, double dt) {
+    const double out = p.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(p.sigma, dw)
+                       : p.diffusion_kind == QRMC_DIFFUSION_DIAG ? DMUL(p.sig[l], dw)
+                                                                  : dw;
+    if (p.drift_kind == QRMC_DRIFT_CONST) return DADD(xo, DADD(DMUL(p.drift_c, dt), out));
+    if (p.drift_kind == QRMC_DRIFT_AFFINE)
+        return DADD(xo, DADD(DMUL(DADD(p.drift_a[l], DMUL(p.drift_b[l], xo)), dt), out));
+    return DADD(xo, out);
+}
+
 // euler_step in place (sde.cpp:37-73); device diffusions have brownian_dim == D.
 // Returns 0 or the SimulationError step.
 template <int D>
@@ -213,12 +230,7 @@ __device__ __forceinline__ int euler_step(const ProblemDev& p, double* x, double
     int bad = 0;
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double out = p.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(p.sigma, dw[l]) : dw[l];
-        double v;
-        if (p.drift_kind == QRMC_DRIFT_CONST)
-            v = DADD(x[l], DADD(DMUL(p.drift_c, dt), out));
-        else
-            v = DADD(x[l], out);
+        const double v = euler_coord(p, x[l], dw[l], l, dt);
         x[l] = v;
         if (!isfinite(v) || fabs(v) > p.state_bound) bad = j + 1;
     }

@@ -45,7 +45,8 @@ constexpr int k1_lt(int d) { return d == 4 ? QRMC_K1_LT_D4 : d <= 2 ? 32 : 8; }
 
 // Product Student-t measure for mu in {1, 2} (proj/src/student.cpp:53-106).
 struct MeasureDev {
-    int form;  // 1 Cauchy, 2 algebraic mu=2
+    int form;  // 1 Cauchy, 2 algebraic mu=2, 3 general mu (include/qrmc_student_t.h)
+    double mu, sqrt_mu;
     double center[kMaxDim];
 };
 
@@ -56,6 +57,7 @@ struct ProblemDev {
     double horizon;
     int terminal_kind, driver_kind, drift_kind, diffusion_kind;
     double tp0, tp1, dp0, dp1, drift_c, sigma;
+    double drift_a[kMaxDim], drift_b[kMaxDim], sig[kMaxDim];  // AFFINE drift a + b x_l, DIAG sigma_l
     double lstar_base;  // C_eta (C_g + T C_f) exp(C_eta L_f T), host-computed exactly as sde.cpp:28-29
     double eta;         // max(eta_g, eta_f)
     double state_bound;

@@ -308,10 +308,8 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
             const double nrm = qrmc_normal_quantile(
                 u64_to_uniform(stream_u64_at(a.seed, tsid, static_cast<uint64_t>(D) * (jj - a.step + 1) + tl)));
             const double dw = DMUL(a.sqrt_dt, nrm);
-            const double out = a.prob.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(a.prob.sigma, dw) : dw;
             const double xo = sm.x[src][tp][tl];
-            const double v = a.prob.drift_kind == QRMC_DRIFT_CONST ? DADD(xo, DADD(DMUL(a.prob.drift_c, a.dt), out))
-                                                                   : DADD(xo, out);
+            const double v = euler_coord(a.prob, xo, dw, tl, a.dt);
             sm.x[src ^ 1][tp][tl] = v;
             if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[tp] == 0) sm.bad[tp] = jj + 1;
             if (jj + 1 < a.steps) sm.theta[tp][tl] = DMUL(3.14159265358979323846, measure_cdf(a.meas, v, tl));

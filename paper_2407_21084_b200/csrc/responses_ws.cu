@@ -399,10 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             const double nrm = 0.001 * (j + l);
 #endif
             const double dw = DMUL(a.sqrt_dt, nrm);
-            const double out = a.prob.diffusion_kind == QRMC_DIFFUSION_SCALAR ? DMUL(a.prob.sigma, dw) : dw;
             const double xo = sm.x[src][p][l];
-            const double v = a.prob.drift_kind == QRMC_DRIFT_CONST ? DADD(xo, DADD(DMUL(a.prob.drift_c, a.dt), out))
-                                                                   : DADD(xo, out);
+            const double v = euler_coord(a.prob, xo, dw, l, a.dt);
             sm.x[src ^ 1][p][l] = v;
             if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[p] == 0) sm.bad[p] = j + 1;
         }

@@ -55,6 +55,28 @@ CASES = [
          growth_f=1.0, lipschitz_f=2.0),
 ]
 
+# row f4: general-mu Student measure (Boost students_t restated in include/qrmc_student_t.h,
+# used by the reference build's shim too) and per-coordinate drift / diagonal sigma functors
+F4_CASES = [
+    dict(name="sin_d2_hyp6_mu3.5", problem="sin", dim=2, kind=2, degrees=(6,), steps=4, paths=3000,
+         damping=2.1, seed=31, mu=3.5),
+    dict(name="sin_d3_total5_mu0.7_center", problem="sin", dim=3, kind=1, degrees=(5,), steps=3, paths=2500,
+         damping=2.1, seed=32, mu=0.7, center=(0.3, -0.2, 0.1)),
+    dict(name="sin_d4_hyp12_mu6", problem="sin", dim=4, kind=2, degrees=(12,), steps=3, paths=2048,
+         damping=5.1, seed=33, mu=6.0),
+    dict(name="ou_affine_diag_d3", problem="custom", dim=3, kind=2, degrees=(8,), steps=4, paths=3000,
+         damping=2.1, seed=34, terminal=_abi.TERMINAL_SIN_SUM, terminal_params=(0.6, 0.577),
+         driver=_abi.DRIVER_SIN_BENCH, driver_params=(0.6, 0.577), drift=_abi.DRIFT_AFFINE,
+         drift_vec=(0.1, -0.2, 0.05, 0, 0, 0, 0, 0, -0.5, -0.3, -1.0, 0, 0, 0, 0, 0),
+         diffusion=_abi.DIFFUSION_DIAG, diffusion_vec=(0.8, 1.1, 0.6), growth_g=2.6, growth_f=1.0,
+         lipschitz_f=2.0),
+    dict(name="affine_diag_d2_mu3", problem="custom", dim=2, kind=0, degrees=(5, 5), steps=3, paths=2000,
+         damping=0.0, seed=35, mu=3.0, terminal=_abi.TERMINAL_X0, driver=_abi.DRIVER_Y,
+         drift=_abi.DRIFT_AFFINE, drift_vec=(0.2, 0.0, 0, 0, 0, 0, 0, 0, 0.1, -0.4, 0, 0, 0, 0, 0, 0),
+         diffusion=_abi.DIFFUSION_DIAG, diffusion_vec=(1.3, 0.5), growth_g=1.0, growth_exp_g=1.0,
+         growth_f=1.0, lipschitz_f=1.0),
+]
+
 PATH_CASES = [
     dict(name="paths_sin_d2", problem="sin", dim=2, kind=2, degrees=(6,), steps=5, paths=10, damping=0.0,
          seed=42, step=1, first=0, n=6),
@@ -78,7 +100,8 @@ def build_case(case: dict):
             dim, case["terminal"], case["driver"], terminal_params=case.get("terminal_params", ()),
             driver_params=case.get("driver_params", ()), drift=case.get("drift", _abi.DRIFT_ZERO),
             drift_params=case.get("drift_params", ()), diffusion=case.get("diffusion", _abi.DIFFUSION_IDENTITY),
-            diffusion_params=case.get("diffusion_params", ()), growth_g=case.get("growth_g", 0.0),
+            diffusion_params=case.get("diffusion_params", ()), drift_vec=case.get("drift_vec", ()),
+            diffusion_vec=case.get("diffusion_vec", ()), growth_g=case.get("growth_g", 0.0),
             growth_exp_g=case.get("growth_exp_g", 0.0), growth_f=case.get("growth_f", 0.0),
             lipschitz_f=case.get("lipschitz_f", 0.0))
     cfg = _abi.ConfigHolder(steps=case["steps"], paths=case["paths"], damping=case["damping"],

@@ -82,8 +82,8 @@ def _solve_status(prob, cfg):
     (dict(paths=0), _abi.EINVAL, "paths must be >= 1"),
     (dict(damping=-1.0), _abi.EINVAL, "damping must be finite"),
     (dict(paths=1 << 40), _abi.EINVAL, "stream-id layout"),
-    (dict(mu=3.5), _abi.ENOTIMPL, "mu must be 1 or 2"),
     (dict(mu=-1.0), _abi.EINVAL, "mu must be positive"),
+    (dict(mu=float("inf")), _abi.EINVAL, "mu must be positive"),
 ])
 def test_config_validation_before_device(bad, status, msg):
     """RunConfig::validate / SamplingMeasure rules (solver.cpp:23-35, student.cpp:21-44)
