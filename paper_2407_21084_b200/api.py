@@ -69,7 +69,8 @@ def _err():
 # ---------------------------------------------------------------- plugin surface
 @dataclass(frozen=True)
 class Measure:
-    """SamplingMeasure (proj/include/qrmc/student.hpp:23-61); mu in {1, 2} on device."""
+    """SamplingMeasure (proj/include/qrmc/student.hpp:23-61): any mu > 0 on the device (mu = 1, 2
+    closed forms; general mu through include/qrmc_student_t.h)."""
 
     mu: float
     dim: int
