@@ -33,6 +33,15 @@
 #include <math.h>
 #endif
 
+/* The general-mu path is rare and long (continued fractions, Newton): on the device it is
+ * kept out of line so it cannot inflate the register allocation of the kernels that
+ * merely contain it (K2's recompute branch spilled 1.7 KB per thread when it was inlined). */
+#if defined(__CUDACC__)
+#define QRMC_HD_COLD static __host__ __device__ __noinline__
+#else
+#define QRMC_HD_COLD static
+#endif
+
 #define QRMC_T_CF_ITERS 300
 #define QRMC_T_NEWTON_ITERS 60
 
@@ -83,7 +92,7 @@ QRMC_HD double qrmc_student_lower(double t, double nu) {
 }
 
 /* F_T(t) for nu degrees of freedom (boost::math::cdf(students_t(nu), t)) */
-QRMC_HD double qrmc_student_cdf(double t, double nu) {
+QRMC_HD_COLD double qrmc_student_cdf(double t, double nu) {
     if (!(t == t)) return t;
     const double lo = qrmc_student_lower(t, nu);
     return t < 0.0 ? lo : 1.0 - lo;
@@ -100,7 +109,7 @@ QRMC_HD double qrmc_student_pdf(double t, double nu) {
  * in t, so Newton in log t converges in a few steps even at p = 1e-15, nu < 1), started
  * inside a bracket found by factor-4 steps from a Cornish-Fisher guess and safeguarded by
  * geometric bisection of that bracket. */
-QRMC_HD double qrmc_student_quantile(double u, double nu) {
+QRMC_HD_COLD double qrmc_student_quantile(double u, double nu) {
     if (u == 0.5) return 0.0;
     const double p = u < 0.5 ? u : 1.0 - u;
     const double lp = log(p);

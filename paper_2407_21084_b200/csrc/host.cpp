@@ -1290,9 +1290,14 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                     m.kmax[l] = pa.kmax[l];
                 }
                 cuda_check(configure_responses_mma(d, smem), "k_responses_mma attributes");
-                // the warp-specialised K1 when two table buffers fit (QRMC_K1=mma keeps k_responses_mma)
+                // the warp-specialised K1 when two table buffers fit and d <= 4: with five or
+                // more coordinates its four producer warps run two Euler/table rounds per
+                // evaluation and the single-buffered k_responses_mma is faster (d=5: 0.111 vs
+                // 0.145 s, d=6 Gamma_H(6,64): 1.02 vs 1.23 s at M=2e6; profiles/r02_k1_ws.md).
+                // QRMC_K1=mma / QRMC_K1=ws force either.
                 const size_t wsmem = responses_ws_smem_bytes(d, off);
-                if (!(k1 && std::strcmp(k1, "mma") == 0) && wsmem && wsmem <= static_cast<size_t>(optin) &&
+                const bool ws_pick = k1 && std::strcmp(k1, "ws") == 0 ? true : (d <= 4 && !(k1 && std::strcmp(k1, "mma") == 0));
+                if (ws_pick && wsmem && wsmem <= static_cast<size_t>(optin) &&
                     static_cast<int64_t>(off) * 32 < 0xFFFF) {
                     MmaLayoutOpts o;
                     o.warps = kWsConsumers;

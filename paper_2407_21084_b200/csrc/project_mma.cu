@@ -66,7 +66,7 @@ __device__ __forceinline__ Batch lane_batch(const StepArgs& a, int lane_rel, int
 }  // namespace
 
 // The batch loop of one warp shape: NG group blocks x up to 8 / NG term blocks.
-template <int D, int NG>
+template <int D, int NG, bool GEN>
 __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArgs& p, ProjSmem& sm, double* tabs0,
                                              size_t tab_elems, int lane_rel, int slot, int4 rc) {
     constexpr int NT = kProjTiles / NG;
@@ -116,12 +116,12 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
                     xl = a.cloud[tl * a.n_owned + bt.q0 + pt];
                 } else {
                     // recompute-from-seeds (solver.cpp:187-193): regenerate X_i
-                    xl = measure_inv_cdf(a.meas,
+                    xl = measure_inv_cdf<GEN>(a.meas,
                                          u64_to_uniform(stream_u64_at(
                                              a.seed, sid_training(a.step, static_cast<uint64_t>(bt.m0 + pt)), tl)),
                                          tl);
                 }
-                c1 = cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, xl, tl)));
+                c1 = cos(DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, xl, tl)));
             }
             if (tq == 0 && tl == 0) sv = a.resp[bt.q0 + pt];
         }
@@ -198,7 +198,7 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
             }
 }
 
-template <int D>
+template <int D, bool GEN>
 __global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, const ProjMmaArgs p) {
     static_assert(D >= 3, "the tensor-core K2 needs an upper prefix");
     static_assert(kProjBatch % 4 == 0 && kChunk % kProjBatch == 0, "batches of whole k-steps inside chunks");
@@ -215,18 +215,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, c
     // sets its register tile. Empty slots carry tiles = 0 and write nothing.
     switch (rc.z & 0xFF) {
         case 16:
-            if constexpr (kProjTiles >= 16) project_rect<D, 16>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 16) project_rect<D, 16, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
         case 8:
-            if constexpr (kProjTiles >= 8) project_rect<D, 8>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 8) project_rect<D, 8, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
         case 4:
-            if constexpr (kProjTiles >= 4) project_rect<D, 4>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 4) project_rect<D, 4, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
         case 2:
-            if constexpr (kProjTiles >= 2) project_rect<D, 2>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 2) project_rect<D, 2, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
-        default: project_rect<D, 1>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
+        default: project_rect<D, 1, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
     }
 }
 
@@ -235,28 +235,30 @@ size_t project_mma_smem_bytes(int table_len) {
 }
 
 template <class Fn>
-static cudaError_t with_project_kernel(int dim, Fn&& fn) {
+static cudaError_t with_project_kernel(int dim, bool gen, Fn&& fn) {
     switch (dim) {
-        case 3: return fn(k_project_mma<3>);
-        case 4: return fn(k_project_mma<4>);
-        case 5: return fn(k_project_mma<5>);
-        case 6: return fn(k_project_mma<6>);
-        case 7: return fn(k_project_mma<7>);
-        case 8: return fn(k_project_mma<8>);
+        case 3: return gen ? fn(k_project_mma<3, true>) : fn(k_project_mma<3, false>);
+        case 4: return gen ? fn(k_project_mma<4, true>) : fn(k_project_mma<4, false>);
+        case 5: return gen ? fn(k_project_mma<5, true>) : fn(k_project_mma<5, false>);
+        case 6: return gen ? fn(k_project_mma<6, true>) : fn(k_project_mma<6, false>);
+        case 7: return gen ? fn(k_project_mma<7, true>) : fn(k_project_mma<7, false>);
+        case 8: return gen ? fn(k_project_mma<8, true>) : fn(k_project_mma<8, false>);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t configure_project_mma(int dim, size_t smem) {
-    return with_project_kernel(dim, [&](auto kern) {
+    auto set = [&](auto kern) {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    });
+    };
+    const cudaError_t e = with_project_kernel(dim, false, set);
+    return e != cudaSuccess ? e : with_project_kernel(dim, true, set);
 }
 
 cudaError_t launch_project_mma(const StepArgs& a, const ProjMmaArgs& p, cudaStream_t st) {
     if (a.owned_lanes == 0 || p.parts == 0) return cudaSuccess;
     const dim3 grid(static_cast<unsigned>(p.parts), static_cast<unsigned>(a.owned_lanes));
-    return with_project_kernel(a.prob.dim, [&](auto kern) {
+    return with_project_kernel(a.prob.dim, a.meas.form == 3, [&](auto kern) {
         kern<<<grid, kThreads, project_mma_smem_bytes(p.table_len), st>>>(a, p);
         return cudaGetLastError();
     });

@@ -92,15 +92,21 @@ __device__ __forceinline__ uint64_t sid_evaluation(int step, uint64_t point) {
 // Product Student-t measure for mu in {1, 2} (proj/src/student.cpp:53-106).
 
 
-// centered_cdf + center shift (student.cpp:53-63, 78-82)
+// centered_cdf + center shift (student.cpp:53-63, 78-82). GEN = false compiles the
+// general-mu branch out: the hot tensor-core kernels are instantiated both ways and the
+// plan picks the general one only for mu not in {1, 2} (a call to the out-of-line
+// Student's t code would otherwise force their register state across a call).
+template <bool GEN = true>
 __device__ __forceinline__ double measure_cdf(const MeasureDev& m, double x, int l) {
     x = DSUB(x, m.center[l]);
     if (m.form == 1) return DADD(0.5, DDIV(atan(x), 3.14159265358979323846));
-    if (m.form == 3) return qrmc_student_cdf(DMUL(x, m.sqrt_mu), m.mu);  // cdf(students_t(mu), x sqrt(mu))
+    if constexpr (GEN)
+        if (m.form == 3) return qrmc_student_cdf(DMUL(x, m.sqrt_mu), m.mu);  // cdf(students_t(mu), x sqrt(mu))
     return DMUL(0.5, DADD(DDIV(x, __dsqrt_rn(DADD(DMUL(x, x), 1.0))), 1.0));
 }
 
 // inv_cdf with the 1e-15 guard band (student.cpp:65-76, 84-89)
+template <bool GEN = true>
 __device__ __forceinline__ double measure_inv_cdf(const MeasureDev& m, double u, int l) {
     const double g = 1e-15;
     u = u < g ? g : u;
@@ -108,7 +114,7 @@ __device__ __forceinline__ double measure_inv_cdf(const MeasureDev& m, double u,
     double c;
     if (m.form == 1)
         c = tan(DMUL(3.14159265358979323846, DSUB(u, 0.5)));
-    else if (m.form == 3)
+    else if (GEN && m.form == 3)
         c = DDIV(qrmc_student_quantile(u, m.mu), m.sqrt_mu);  // quantile(students_t(mu), u) / sqrt(mu)
     else
         c = DDIV(DSUB(u, 0.5), __dsqrt_rn(DMUL(u, DSUB(1.0, u))));

@@ -239,7 +239,7 @@ __device__ __forceinline__ void run_unit(const MmaArgs& m, int cb0, int c0, int 
 
 }  // namespace
 
-template <int D>
+template <int D, bool GEN>
 #ifndef QRMC_MMA_MINB
 #define QRMC_MMA_MINB 1
 #endif
@@ -282,10 +282,10 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
     const int64_t tq = q0 + tp;
     const uint64_t tsid = sid_training(a.step, static_cast<uint64_t>(owned_path(a, tq < a.n_owned ? tq : 0)));
     if (task) {
-        const double x = measure_inv_cdf(a.meas, u64_to_uniform(stream_u64_at(a.seed, tsid, tl)), tl);
+        const double x = measure_inv_cdf<GEN>(a.meas, u64_to_uniform(stream_u64_at(a.seed, tsid, tl)), tl);
         sm.x[0][tp][tl] = x;
         if (a.cloud && tq < a.n_owned)
-            a.cloud[tl * a.n_owned + tq] = a.cloud_cos ? cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, x, tl))) : x;
+            a.cloud[tl * a.n_owned + tq] = a.cloud_cos ? cos(DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, x, tl))) : x;
     }
     __syncthreads();
     uint32_t apps = 0, clipped = 0;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, QRMC_MMA_MINB) k_responses_mma(const
             const double v = euler_coord(a.prob, xo, dw, tl, a.dt);
             sm.x[src ^ 1][tp][tl] = v;
             if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[tp] == 0) sm.bad[tp] = jj + 1;
-            if (jj + 1 < a.steps) sm.theta[tp][tl] = DMUL(3.14159265358979323846, measure_cdf(a.meas, v, tl));
+            if (jj + 1 < a.steps) sm.theta[tp][tl] = DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, v, tl));
         }
     };
     // x-only parts of evaluation jj (path p), one kind per task so that the
@@ -517,29 +517,31 @@ size_t responses_mma_smem_bytes(int dim, int table_len) {
 }
 
 template <class Fn>
-static cudaError_t with_kernel(int dim, Fn&& fn) {
+static cudaError_t with_kernel(int dim, bool gen, Fn&& fn) {
     switch (dim) {
-        case 3: return fn(k_responses_mma<3>);
-        case 4: return fn(k_responses_mma<4>);
-        case 5: return fn(k_responses_mma<5>);
-        case 6: return fn(k_responses_mma<6>);
-        case 7: return fn(k_responses_mma<7>);
-        case 8: return fn(k_responses_mma<8>);
+        case 3: return gen ? fn(k_responses_mma<3, true>) : fn(k_responses_mma<3, false>);
+        case 4: return gen ? fn(k_responses_mma<4, true>) : fn(k_responses_mma<4, false>);
+        case 5: return gen ? fn(k_responses_mma<5, true>) : fn(k_responses_mma<5, false>);
+        case 6: return gen ? fn(k_responses_mma<6, true>) : fn(k_responses_mma<6, false>);
+        case 7: return gen ? fn(k_responses_mma<7, true>) : fn(k_responses_mma<7, false>);
+        case 8: return gen ? fn(k_responses_mma<8, true>) : fn(k_responses_mma<8, false>);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t configure_responses_mma(int dim, size_t smem) {
-    return with_kernel(dim, [&](auto kern) {
+    auto set = [&](auto kern) {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    });
+    };
+    const cudaError_t e = with_kernel(dim, false, set);
+    return e != cudaSuccess ? e : with_kernel(dim, true, set);
 }
 
 cudaError_t launch_responses_mma(const StepArgs& a, const MmaArgs& m, cudaStream_t st) {
     if (a.n_owned == 0) return cudaSuccess;
     const size_t smem = responses_mma_smem_bytes(a.prob.dim, m.table_len);
     const unsigned blocks = static_cast<unsigned>((a.n_owned + kMmaPaths - 1) / kMmaPaths);
-    const cudaError_t e = with_kernel(a.prob.dim, [&](auto kern) {
+    const cudaError_t e = with_kernel(a.prob.dim, a.meas.form == 3, [&](auto kern) {
         kern<<<blocks, kThreads, smem, st>>>(a, m);
         return cudaGetLastError();
     });

@@ -260,7 +260,7 @@ __device__ __forceinline__ void ws_unit(const WsArgs& m, int cb0, int c0, int c1
 
 }  // namespace
 
-template <int D>
+template <int D, bool GEN>
 __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, const WsArgs m) {
     static_assert(D >= 3, "the tensor-core K1 needs an upper prefix");
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -341,10 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
 
     // start points X_i ~ nu: draws 0..D-1 of the path's stream (solver.cpp:150-152)
     for (int l = pw; l < D; l += kWsProducers) {
-        const double x = measure_inv_cdf(a.meas, u64_to_uniform(stream_u64_at(a.seed, sid, l)), l);
+        const double x = measure_inv_cdf<GEN>(a.meas, u64_to_uniform(stream_u64_at(a.seed, sid, l)), l);
         sm.x[0][p][l] = x;
         if (a.cloud && live)
-            a.cloud[l * a.n_owned + q] = a.cloud_cos ? cos(DMUL(3.14159265358979323846, measure_cdf(a.meas, x, l))) : x;
+            a.cloud[l * a.n_owned + q] = a.cloud_cos ? cos(DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, x, l))) : x;
     }
     bar_sync(kBarProd, kProdThreads);
     if (pw == 0) {
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             bar_sync(kBarProd, kProdThreads);
             double* tb = tabs + (j & 1) * tab_elems;
             for (int l = pw; l < D; l += kWsProducers) {
-                const double th = DMUL(3.14159265358979323846, measure_cdf(a.meas, sm.x[src ^ 1][p][l], l));
+                const double th = DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, sm.x[src ^ 1][p][l], l));
 #ifndef QRMC_WS_EXP_NOTAB
                 ws_table(th, m.kmax[l], m.offset[l], p, tb);
 #else
@@ -514,29 +514,31 @@ size_t responses_ws_smem_bytes(int dim, int table_len) {
 }
 
 template <class Fn>
-static cudaError_t with_ws_kernel(int dim, Fn&& fn) {
+static cudaError_t with_ws_kernel(int dim, bool gen, Fn&& fn) {
     switch (dim) {
-        case 3: return fn(k_responses_ws<3>);
-        case 4: return fn(k_responses_ws<4>);
-        case 5: return fn(k_responses_ws<5>);
-        case 6: return fn(k_responses_ws<6>);
-        case 7: return fn(k_responses_ws<7>);
-        case 8: return fn(k_responses_ws<8>);
+        case 3: return gen ? fn(k_responses_ws<3, true>) : fn(k_responses_ws<3, false>);
+        case 4: return gen ? fn(k_responses_ws<4, true>) : fn(k_responses_ws<4, false>);
+        case 5: return gen ? fn(k_responses_ws<5, true>) : fn(k_responses_ws<5, false>);
+        case 6: return gen ? fn(k_responses_ws<6, true>) : fn(k_responses_ws<6, false>);
+        case 7: return gen ? fn(k_responses_ws<7, true>) : fn(k_responses_ws<7, false>);
+        case 8: return gen ? fn(k_responses_ws<8, true>) : fn(k_responses_ws<8, false>);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t configure_responses_ws(int dim, size_t smem) {
-    return with_ws_kernel(dim, [&](auto kern) {
+    auto set = [&](auto kern) {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    });
+    };
+    const cudaError_t e = with_ws_kernel(dim, false, set);
+    return e != cudaSuccess ? e : with_ws_kernel(dim, true, set);
 }
 
 cudaError_t launch_responses_ws(const StepArgs& a, const WsArgs& m, cudaStream_t st) {
     if (a.n_owned == 0) return cudaSuccess;
     const size_t smem = responses_ws_smem_bytes(a.prob.dim, m.table_len);
     const unsigned blocks = static_cast<unsigned>((a.n_owned + kWsPaths - 1) / kWsPaths);
-    return with_ws_kernel(a.prob.dim, [&](auto kern) {
+    return with_ws_kernel(a.prob.dim, a.meas.form == 3, [&](auto kern) {
         kern<<<blocks, kThreads, smem, st>>>(a, m);
         return cudaGetLastError();
     });

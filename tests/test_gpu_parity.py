@@ -273,7 +273,8 @@ def test_series_program_kernels_match_reference(L, entry, monkeypatch):
 def test_tensor_core_kernels_selected(L, dim, kind, deg):
     prob = _abi.sin_bench_problem(dim)
     cfg = _abi.ConfigHolder(steps=3, paths=2048, damping=5.1, seed=1, gamma_kind=kind, degrees=deg)
-    assert _kernel_names(prob, cfg) == ["k_responses_ws", "k_project_mma", "k_finish_step"]
+    k1 = "k_responses_ws" if dim <= 4 else "k_responses_mma"  # host.cpp make_plan policy
+    assert _kernel_names(prob, cfg) == [k1, "k_project_mma", "k_finish_step"]
 
 
 @pytest.mark.parametrize("entry", [e for e in GOLDEN["solves"] if e["case"]["dim"] >= 3],
@@ -289,6 +290,19 @@ def test_ring_tensor_core_k1_matches_reference(L, entry, monkeypatch):
     ref = unhex(entry["coeffs"]).reshape(coeffs.shape)
     assert alpha_close(coeffs, ref) <= ALPHA_TOL
     assert (stats.applications, stats.clipped) == (entry["applications"], entry["clipped"])
+
+
+@pytest.mark.parametrize("dim,deg", [(5, 12), (6, 8)])
+def test_forced_ws_k1_matches_port_for_more_coordinates(L, port, monkeypatch, dim, deg):
+    # the warp-specialised K1 stays correct where the plan prefers k_responses_mma
+    monkeypatch.setenv("QRMC_K1", "ws")
+    prob = _abi.sin_bench_problem(dim)
+    cfg = _abi.ConfigHolder(steps=3, paths=4000, damping=5.1, seed=21, gamma_kind=2, degrees=[deg])
+    assert _kernel_names(prob, cfg)[0] == "k_responses_ws"
+    coeffs, stats, _ = api.backward_solve(prob, cfg)
+    ref, rs = port.backward_solve(prob, cfg, coeffs.shape[1])
+    assert alpha_close(coeffs, ref) <= ALPHA_TOL
+    assert stats.applications == rs.applications
 
 
 def test_ws_and_ring_k1_agree_at_config2_shape(L, monkeypatch):

@@ -30,10 +30,12 @@ plan = C.c_void_p()
 err = C.create_string_buffer(1024)
 api.raise_for(L.qrmc_gpu_plan_create(None, C.byref(prob), cfg.ref(), C.byref(plan), err, 1024), err.value.decode())
 st = _abi.Stats()
-for _ in range(args.runs):
-    api.raise_for(L.qrmc_gpu_plan_run(plan, C.byref(st), err, 1024), err.value.decode(), st.error_step)
 ks = (C.c_double * 3)()
-L.qrmc_gpu_plan_kernel_seconds(plan, ks, None, err, 1024)
+for r in range(args.runs):
+    api.raise_for(L.qrmc_gpu_plan_run(plan, C.byref(st), err, 1024), err.value.decode(), st.error_step)
+    L.qrmc_gpu_plan_kernel_seconds(plan, ks, None, err, 1024)
+    if args.runs > 1:
+        print(json.dumps({"run": r, "kernel_seconds": ks[:]}), flush=True)
 K = L.qrmc_gpu_plan_basis_size(plan)
 n, m = args.steps, args.paths
 names = [L.qrmc_gpu_plan_kernel_name(plan, w).decode() for w in range(3)]
