@@ -15,7 +15,7 @@
  * Scheme (explicit one-step SRMC, backward i = N-1 .. 0, t_i = i*dt):
  *   for every cell k and path m < M of step i (stream id (i << 40) | (k*M + m)):
  *     X_i      = lo + (c(k) + U) * h               U: d uniforms (rng.hpp:41-43)
- *     dW       = sqrt(dt) * Z                      Z: d normals (rng.cpp:42-49)
+ *     dW       = sqrt(dt) * Z                      Z = PPND16(U): d normals (AS241, qrmc_normal_quantile.h)
  *     X_{i+1}  = X_i + b(X_i) dt + sigma dW        (sde.cpp:37-73, diagonal sigma)
  *     Y1       = i+1 == N ? g(X_{i+1}) : clamp(yhat_{i+1}(X_{i+1}), +-L)
  *     Zhat_i   = LS fit in cell k of Y1 * dW / dt   (only when the driver uses z or want_z)

@@ -82,7 +82,7 @@ static void s_path(const srmc_t* s, const double* next, const int* cc, int step,
         if (s->P > 1) phi[1 + l] = 2.0 * u - 1.0;
     }
     for (int l = 0; l < s->d; ++l) {
-        dw[l] = s->sqrt_dt * stream_normal(&r);
+        dw[l] = s->sqrt_dt * qrmc_ppnd16(stream_uniform(&r)); /* PPND16 directly, as the device */
         x1[l] = (x0[l] + s->bdt) + s->sig * dw[l];
     }
     if (s->last) {

@@ -49,7 +49,13 @@ constexpr int kRB = kWsPaths / 8;  // row blocks
 #endif
 constexpr int kWsConsumerRegs = QRMC_WS_CONSUMER_REGS;
 constexpr int kWsProducerRegs = QRMC_WS_PRODUCER_REGS;
-static_assert(kWsConsumers * kWsConsumerRegs + kWsProducers * kWsProducerRegs <= 65536 / 32, "register file");
+// setmaxnreg only moves registers inside the CTA's launch allocation (ptxas allocates
+// 65536 / kThreads rounded down to 8 per thread): a larger total would leave the
+// consumers' setmaxnreg.inc waiting forever
+constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8;
+static_assert(kWsConsumers * kWsConsumerRegs + kWsProducers * kWsProducerRegs <=
+                  (kWsConsumers + kWsProducers) * kLaunchRegs,
+              "setmaxnreg budget exceeds the launch allocation");
 static_assert(kRB == 4, "the swizzled operand addressing assumes 4 row blocks");
 static_assert(kWsConsumers % 4 == 0 && kWsProducers == 4, "one producer warp per SM sub-partition");
 

@@ -155,7 +155,11 @@ __device__ __forceinline__ void chol_solve(const double* A, double* b) {
 
 // The quantile is called 2-pass x D times per path; one out-of-line copy keeps the
 // kernel's instruction footprint small (bit-identical arithmetic).
-__device__ __noinline__ double srmc_normal_quantile(double u) { return qrmc_normal_quantile(u); }
+// SRMC's Gaussian increments are PPND16(u) itself (AS241, include/qrmc_normal_quantile.h):
+// the reference's composition -sqrt(2) * erfc_inv(2u) = -sqrt(2) * (-PPND16(u) / sqrt(2))
+// adds a division and a multiplication that only matter for bit parity with the GQRMDP
+// reference path; SRMC's draws are its own (oracle/srmc_oracle.c does the same).
+__device__ __noinline__ double srmc_normal_quantile(double u) { return qrmc_ppnd16(u); }
 
 // One path of cell k: start X_i (and its local coordinates), dW, endpoint response Y1.
 template <int D, int P>

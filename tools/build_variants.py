@@ -14,11 +14,15 @@ from paper_2407_21084_b200 import build  # noqa: E402
 def one(spec):
     name, _, defs = spec.partition("=")
     out = ROOT / "paper_2407_21084_b200" / "_lib" / "variants" / f"libqrmc_gpu_{name}.so"
-    build.build(out=out, defines=[d for d in defs.split(",") if d], only={"responses_ws.cu"})
+    build.build(out=out, defines=[d for d in defs.split(",") if d], only=ONLY)
     return out
 
 
+ONLY = {"responses_ws.cu"}
+args = sys.argv[1:]
+if args and args[0].startswith("--only="):
+    ONLY = set(args.pop(0)[len("--only="):].split(","))
 build.build()  # the main objects the variants link against
 with ThreadPoolExecutor(max_workers=4) as ex:
-    for p in ex.map(one, sys.argv[1:]):
+    for p in ex.map(one, args):
         print(p)
