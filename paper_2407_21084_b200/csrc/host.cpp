@@ -523,6 +523,10 @@ struct MmaLayoutOpts {
     bool euler_ahead = true;    // the first warps also run the Euler steps (responses_mma.cu)
     bool ring = true;           // steps aligned to W slots and warp segments to the cp.async ring
     int bank_order = QRMC_MMA_BANK_ORDER;
+    // the first tail_terms (a multiple of 8) terms of every group go to a transposed GEMM
+    // over the groups (units with nb = 8 + tail_terms / 8, responses_ws.cu ws_unit_t): no
+    // per-unit epilogue for the hyperbolic tail's many small groups
+    int tail_terms = 0;
 };
 
 struct MmaLayout {
@@ -558,6 +562,16 @@ inline uint32_t ws_off(int e, int half, bool second) {
 }
 
 inline int ws_gk_record(int d) { return (2 * (d - 2) + 3) / 4 * 4; }
+// terms of every group the warp-specialised K1 runs as a transposed GEMM (0, 8 or 16;
+// QRMC_WS_TAIL overrides)
+#ifndef QRMC_WS_TAIL_DEFAULT
+#define QRMC_WS_TAIL_DEFAULT 0
+#endif
+inline int ws_tail_terms() {
+    const char* e = std::getenv("QRMC_WS_TAIL");
+    const int v = e ? std::atoi(e) : QRMC_WS_TAIL_DEFAULT;
+    return v == 16 ? 16 : v == 8 ? 8 : 0;
+}
 inline size_t ws_gk_index(int d, int n_groups, int half, int g, int l) {
     return (static_cast<size_t>(half) * (n_groups / 2) + g / 2) * ws_gk_record(d) + (g % 2) * (d - 2) + l;
 }
@@ -635,7 +649,8 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
             if (rank[static_cast<size_t>(at(r, d - 2)) * Bn + at(r, d - 1)] >= gr.n) return L;  // not a prefix
     if (static_cast<int64_t>(offset[d - 1] + Bn) * kMmaTabStride > 0xFFFF) return L;
     auto row_of = [](int entry) { return static_cast<uint32_t>(entry * kMmaTabStride); };
-    const int n_terms = static_cast<int>((order.size() + 7) & ~size_t{7});  // K1 reads 4-term chunks, K2 8-term blocks
+    // K1 reads 4-term chunks, K2 8-term blocks, the transposed tail its first tail_terms terms
+    const int n_terms = std::max(static_cast<int>((order.size() + 7) & ~size_t{7}), opt.tail_terms);
     L.terms.assign(static_cast<size_t>(n_terms), row_of(offset[d - 2]) | row_of(offset[d - 1]) << 16);
     for (size_t t = 0; t < order.size(); ++t)
         L.terms[t] = row_of(offset[d - 2] + order[t] / Bn) | row_of(offset[d - 1] + order[t] % Bn) << 16;
@@ -709,6 +724,14 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
     // processing time first) with an issue-slot cost model
     struct Unit { int cb0, nb, c0, c1; double cost; };
     std::vector<Unit> units;
+    // issue-slot cost model of a unit: per chunk step cost_step + nb cost_nb, per column
+    // block epilogue cost_epi (QRMC_COST_STEP / _NB / _EPI override, tuning only)
+    auto env_or = [](const char* n, double v) {
+        const char* e = std::getenv(n);
+        return e ? std::atof(e) : v;
+    };
+    const double cost_step = env_or("QRMC_COST_STEP", 16.0), cost_nb = env_or("QRMC_COST_NB", 10.0),
+                 cost_epi = env_or("QRMC_COST_EPI", 48.0);
     auto add_units = [&](int cb, int nb, int lo, int hi) {  // chunk range [lo, hi) of cbs cb..cb+nb-1
         if (hi <= lo) return;
         const int np = (hi - lo + kMmaKSplit - 1) / kMmaKSplit;
@@ -716,28 +739,49 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
             const int c0 = lo + static_cast<int>(static_cast<int64_t>(hi - lo) * q / np);
             const int c1 = lo + static_cast<int>(static_cast<int64_t>(hi - lo) * (q + 1) / np);
             const double len = c1 - c0;
-            units.push_back({cb, nb, c0, c1, len * (16.0 + nb * 10.0) + nb * 48.0});
+            units.push_back({cb, nb, c0, c1, len * (cost_step + nb * cost_nb) + nb * cost_epi});
         }
     };
 #ifndef QRMC_MMA_STAIR
 #define QRMC_MMA_STAIR 1
 #endif
-    for (int cb = 0; cb < n_cb;) {
+    // the tail: column blocks whose groups all have <= tail_terms terms (groups are sorted
+    // by size) go to the transposed GEMM over their groups; the rest stay here
+    const int tnb = opt.tail_terms / 8;  // term blocks of the transposed GEMM (N = 8 terms each)
+    int tail_cb = n_cb;
+    if (tnb > 0)
+        for (int cb = 0; cb < n_cb; ++cb)
+            if (4 * cb_chunks[cb] <= opt.tail_terms) {
+                tail_cb = cb;
+                break;
+            }
+    for (int cb = 0; cb < tail_cb;) {
         int e = cb;
         if (QRMC_MMA_STAIR) {
             // staircase bundles: kMmaBundle consecutive column blocks share the chunks
             // all of them have; each block's remainder runs in narrower units
-            e = std::min(n_cb, cb + kMmaBundle);
+            e = std::min(tail_cb, cb + kMmaBundle);
             int lo = 0;
             for (int k = e; k > cb; --k) {  // blocks cb..k-1 share [lo, E_{k-1})
                 add_units(cb, k - cb, lo, cb_chunks[k - 1]);
                 lo = std::max(lo, cb_chunks[k - 1]);
             }
         } else {
-            while (e < n_cb && e - cb < kMmaBundle && cb_chunks[e] == cb_chunks[cb]) ++e;
+            while (e < tail_cb && e - cb < kMmaBundle && cb_chunks[e] == cb_chunks[cb]) ++e;
             add_units(cb, e - cb, 0, cb_chunks[cb]);
         }
         cb = e;
+    }
+    // transposed units: chunks of 4 groups (2 n_cb of them) x tnb blocks of 8 terms,
+    // encoded nb = 8 + tnb; cost: A fragments need d-2 table rows per group
+    if (tnb > 0 && tail_cb < n_cb) {
+        const int tb = 2 * tail_cb, tc = 2 * n_cb - tb;  // chunks of 4 groups: [tb, 2 n_cb)
+        const int np = (tc + kMmaKSplit - 1) / kMmaKSplit;
+        for (int q = 0; q < np; ++q) {
+            const int c0 = tb + static_cast<int>(static_cast<int64_t>(tc) * q / np);
+            const int c1 = tb + static_cast<int>(static_cast<int64_t>(tc) * (q + 1) / np);
+            units.push_back({-1, 8 + tnb, c0, c1, (c1 - c0) * (16.0 + tnb * 10.0 + 4.0 * nu) + tnb * 48.0});
+        }
     }
     std::vector<int32_t> ui(units.size());
     for (size_t i = 0; i < ui.size(); ++i) ui[i] = static_cast<int32_t>(i);
@@ -789,6 +833,7 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
     }
     std::vector<int64_t> frag_at(static_cast<size_t>(n_cb) * cb_chunks[0], -1);
     const int cstride = cb_chunks[0];
+    std::vector<int64_t> tfrag_at(static_cast<size_t>(2 * n_cb) * std::max(tnb, 1), -1);  // [tchunk][term block]
     int64_t woff = 0;
     for (int w = 0; w < n_warps; ++w) {
         std::sort(per_warp[w].begin(), per_warp[w].end(), [&](int32_t x, int32_t y) {
@@ -799,6 +844,12 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
         for (int32_t u : per_warp[w]) {
             const Unit& un = units[u];
             L.units.push_back(make_int4(un.cb0, un.nb, un.c0, un.c1));
+            if (un.nb >= 8) {  // transposed: tnb fragments per chunk of 4 groups
+                for (int c = un.c0; c < un.c1; ++c, f += tnb)
+                    for (int i = 0; i < tnb; ++i) tfrag_at[static_cast<size_t>(c) * tnb + i] = woff + f + i;
+                L.frags += static_cast<int64_t>(tnb) * (un.c1 - un.c0);
+                continue;
+            }
             // a step takes 1, 2 or 4 fragment slots (3 column blocks use 4), aligned,
             // so no step straddles the ring wrap
             const int stride = opt.ring && un.nb == 3 ? 4 : un.nb;
@@ -820,6 +871,13 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
         const int cb = c / 8, n = c % 8;
         for (int64_t r = gr.r0; r < gr.r0 + gr.n; ++r) {
             const int t = rank[static_cast<size_t>(at(r, d - 2)) * Bn + at(r, d - 1)];
+            if (cb >= tail_cb) {
+                // transposed: B[k = group c % 4][n = term t % 8] of chunk c / 4, block t / 8
+                const int64_t f = tfrag_at[static_cast<size_t>(c / 4) * tnb + t / 8];
+                if (f < 0) fail(QRMC_ELOGIC, "mma layout: tail term outside the fragment stream");
+                L.pos[static_cast<size_t>(r)] = static_cast<int32_t>(f * 32 + (((t % 8) << 2) | (c % 4)));
+                continue;
+            }
             const int64_t f = frag_at[static_cast<size_t>(cb) * cstride + t / 4];
             if (f < 0) fail(QRMC_ELOGIC, "mma layout: term outside the fragment stream");
             L.pos[static_cast<size_t>(r)] = static_cast<int32_t>(f * 32 + ((n << 2) | (t & 3)));
@@ -1304,6 +1362,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                     o.euler_ahead = false;
                     o.ring = false;
                     o.bank_order = 1;
+                    o.tail_terms = ws_tail_terms();
                     MmaLayout W = build_mma_layout(P->gamma, pa.offset, o);
                     if (W.ok) {
                         P->use_ws = true;
@@ -1646,12 +1705,13 @@ qrmc_status qrmc_gpu_mma_layout_check(int32_t kind, int32_t dim, const int32_t* 
         // swizzled [entry][32] tables; replay every lane's operand addressing
         // (row-half offsets, row blocks r = 0..3 at A[0], B[0], A[16], B[16]) and the
         // dense per-warp fragment streams, then compare each path's y with the direct sum
-        {
+        for (int tail : {0, 8, 16}) {
             MmaLayoutOpts o;
             o.warps = kWsConsumers;
             o.euler_ahead = false;
             o.ring = false;
             o.bank_order = 1;
+            o.tail_terms = tail;
             const MmaLayout W = build_mma_layout(g, offset, o);
             if (!W.ok) fail(QRMC_ELOGIC, "ws layout: not a chain although the mma layout is");
             std::vector<double> wtab(static_cast<size_t>(off) * 32, 0.0);
@@ -1684,6 +1744,46 @@ qrmc_status qrmc_gpu_mma_layout_check(int32_t kind, int32_t dim, const int32_t* 
                 int64_t f = wi.z;
                 for (int u = wi.x; u < wi.y; ++u) {
                     const int4 un = W.units[static_cast<size_t>(u)];
+                    if (un.y >= 8) {
+                        // transposed tail unit: K = 4 groups per chunk, N = 8 terms per block;
+                        // A[row][k] = U_{4c+k}(path), B[k][n] at lane n * 4 + k
+                        const int tnb = un.y - 8;
+                        std::vector<double> C(static_cast<size_t>(tnb) * 4 * 64, 0.0);  // [i][r][row][term col]
+                        for (int c = un.z; c < un.w; ++c, f += tnb)
+                            for (int i = 0; i < tnb; ++i)
+                                for (int lane = 0; lane < 32; ++lane) {
+                                    const int row = lane >> 2, col = lane & 3, half = row >> 2;
+                                    double uu[4] = {1, 1, 1, 1};
+                                    for (int l = 0; l < d - 2; ++l) {
+                                        const uint32_t o2 = W.ws_gk[ws_gk_index(d, n_groups, half, 4 * c + col, l)];
+                                        uu[0] *= at_off(lane, o2 & 0xFFFFu, 0);
+                                        uu[1] *= at_off(lane, o2 >> 16, 0);
+                                        uu[2] *= at_off(lane, o2 & 0xFFFFu, 1);
+                                        uu[3] *= at_off(lane, o2 >> 16, 1);
+                                    }
+                                    for (int r = 0; r < 4; ++r)
+                                        for (int n = 0; n < 8; ++n)
+                                            C[((static_cast<size_t>(i) * 4 + r) * 8 + row) * 8 + n] +=
+                                                uu[r] * ws[static_cast<size_t>((f + i) * 32 + n * 4 + col)];
+                                }
+                        for (int i = 0; i < tnb; ++i)
+                            for (int lane = 0; lane < 32; ++lane) {
+                                const int row = lane >> 2, col = lane & 3, half = row >> 2;
+                                for (int h = 0; h < 2; ++h) {
+                                    const int t = 8 * i + 2 * col + h;
+                                    const uint4 tw = W.ws_terms[static_cast<size_t>(t) * 2 + half];
+                                    double a[4];
+                                    a[0] = at_off(lane, tw.x / 8, 0) * at_off(lane, tw.z / 8, 0);
+                                    a[1] = at_off(lane, tw.y / 8, 0) * at_off(lane, tw.w / 8, 0);
+                                    a[2] = at_off(lane, tw.x / 8, 1) * at_off(lane, tw.z / 8, 1);
+                                    a[3] = at_off(lane, tw.y / 8, 1) * at_off(lane, tw.w / 8, 1);
+                                    for (int r = 0; r < 4; ++r)
+                                        yp[static_cast<size_t>(8 * r + row)] +=
+                                            a[r] * C[((static_cast<size_t>(i) * 4 + r) * 8 + row) * 8 + 2 * col + h];
+                                }
+                            }
+                        continue;
+                    }
                     const int nb = un.y;
                     std::vector<double> C(static_cast<size_t>(nb) * 4 * 64, 0.0);  // [i][r][path row][group col]
                     for (int c = un.z; c < un.w; ++c, f += nb)

@@ -264,6 +264,97 @@ __device__ __forceinline__ void ws_unit(const WsArgs& m, int cb0, int c0, int c1
     }
 }
 
+// A transposed tail unit (host.cpp MmaLayoutOpts::tail_terms): chunks [c0, c1) of 4
+// groups, NBT blocks of 8 terms. D_t = sum_u U_u alpha'_{u,t} as DMMAs with the group
+// products U (d-2 table rows per group) as the A operand, then y += A_t D_t for the
+// unit's 8 NBT terms -- one epilogue for many small groups.
+template <int D, int NBT>
+__device__ __forceinline__ void ws_unit_t(const WsArgs& m, int c0, int c1, const double*& bsrc, const char* trow,
+                                          int half, int col, double (&y)[kRB]) {
+    double acc[kRB][NBT][2];
+    constexpr int R = (2 * (D - 2) + 3) / 4 * 4;  // group-pair record (host.cpp ws_gk_index)
+    const uint4* rec = reinterpret_cast<const uint4*>(m.gk) +
+                       (static_cast<size_t>(half) * (m.n_groups / 2) + 2 * c0 + (col >> 1)) * (R / 4);
+    const int sub = (col & 1) * (D - 2);
+    uint32_t wn[R];
+    auto load_rec = [&](uint32_t (&w)[R]) {
+#pragma unroll
+        for (int q = 0; q < R / 4; ++q) {
+            const uint4 v = ldg_keep(rec + q);
+            w[4 * q] = v.x;
+            w[4 * q + 1] = v.y;
+            w[4 * q + 2] = v.z;
+            w[4 * q + 3] = v.w;
+        }
+    };
+    load_rec(wn);
+    auto step = [&](auto first, bool more) {
+        uint32_t w[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) w[q] = wn[q];
+        rec += 2 * (R / 4);  // next chunk: 4 groups = 2 pair records
+        if (more) load_rec(wn);
+        double a[kRB];
+#pragma unroll
+        for (int l = 0; l < D - 2; ++l) {
+            const uint32_t o = w[sub + l];
+            const double* pA = reinterpret_cast<const double*>(trow) + (o & 0xFFFFu);
+            const double* pB = reinterpret_cast<const double*>(trow) + (o >> 16);
+            if (l == 0) {
+                a[0] = pA[0];
+                a[1] = pB[0];
+                a[2] = pA[16];
+                a[3] = pB[16];
+            } else {
+                a[0] = DMUL(a[0], pA[0]);
+                a[1] = DMUL(a[1], pB[0]);
+                a[2] = DMUL(a[2], pA[16]);
+                a[3] = DMUL(a[3], pB[16]);
+            }
+        }
+        double b[NBT];
+#pragma unroll
+        for (int i = 0; i < NBT; ++i) {
+            b[i] = ldg_stream(bsrc + 32 * i);
+            prefetch_l1(bsrc + 32 * (kWsPrefetch + i));
+        }
+        bsrc += 32 * NBT;
+#pragma unroll
+        for (int i = 0; i < NBT; ++i)
+#pragma unroll
+            for (int r = 0; r < kRB; ++r) {
+                if constexpr (decltype(first)::value)
+                    dmma0(acc[r][i], a[r], b[i]);
+                else
+                    dmma(acc[r][i], a[r], b[i]);
+            }
+    };
+    step(std::true_type{}, c0 + 1 < c1);
+    int c = c0 + 1;
+    for (; c + 3 < c1; c += 4) {
+        step(std::false_type{}, true);
+        step(std::false_type{}, true);
+        step(std::false_type{}, true);
+        step(std::false_type{}, c + 4 < c1);
+    }
+    for (; c < c1; ++c) step(std::false_type{}, c + 1 < c1);
+    // epilogue: the lane's terms t = 8 i + 2 col + h, A_t = c_s(x_{d-2}) c_b(x_{d-1})
+#pragma unroll
+    for (int i = 0; i < NBT; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint4 tw = ldg_keep(m.terms + (8 * i + 2 * col + h) * 2 + half);
+            const double* sA = reinterpret_cast<const double*>(trow + tw.x);
+            const double* sB = reinterpret_cast<const double*>(trow + tw.y);
+            const double* bA = reinterpret_cast<const double*>(trow + tw.z);
+            const double* bB = reinterpret_cast<const double*>(trow + tw.w);
+            y[0] = fma(DMUL(sA[0], bA[0]), acc[0][i][h], y[0]);
+            y[1] = fma(DMUL(sB[0], bB[0]), acc[1][i][h], y[1]);
+            y[2] = fma(DMUL(sA[16], bA[16]), acc[2][i][h], y[2]);
+            y[3] = fma(DMUL(sB[16], bB[16]), acc[3][i][h], y[3]);
+        }
+}
+
 }  // namespace
 
 template <int D, bool GEN>
@@ -312,8 +403,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
                 const int4 un = ldg_keep(&m.units[u]);
                 if (un.y == 1)
                     ws_unit<D, 1>(m, un.x, un.z, un.w, bsrc, trow, half, col, y);
-                else
+                else if (un.y == 2)
                     ws_unit<D, 2>(m, un.x, un.z, un.w, bsrc, trow, half, col, y);
+                else if (un.y == 9)
+                    ws_unit_t<D, 1>(m, un.z, un.w, bsrc, trow, half, col, y);
+                else
+                    ws_unit_t<D, 2>(m, un.z, un.w, bsrc, trow, half, col, y);
             }
 #pragma unroll
             for (int r = 0; r < kRB; ++r) {
