@@ -68,6 +68,7 @@ __device__ __forceinline__ double srmc_driver(const SrmcDev& s, const double* x,
 template <int D, int P>
 __device__ __forceinline__ double srmc_eval(const SrmcDev& s, const double* __restrict__ tab, const double* x) {
     int64_t k = 0;
+    int cs[D];
     double sl[D];
 #pragma unroll
     for (int l = 0; l < D; ++l) {
@@ -75,10 +76,12 @@ __device__ __forceinline__ double srmc_eval(const SrmcDev& s, const double* __re
         xc = xc > s.hi ? s.hi : xc;
         int c = static_cast<int>(floor(DMUL(DSUB(xc, s.lo), s.inv_h)));  // the reciprocal, as the oracle
         c = c < 0 ? 0 : (c >= s.n ? s.n - 1 : c);
+        cs[l] = c;
         k = k * s.n + c;
         const double centre = DADD(s.lo, DMUL(DADD(static_cast<double>(c), 0.5), s.h));
         sl[l] = DMUL(DSUB(xc, centre), s.inv2h);
     }
+    if (s.morton) k = morton_encode<D>(cs, s.mmul, s.mmask);
     const double* row = tab + k * P;
     double v = __ldg(row);
     if constexpr (P > 1) {
@@ -232,12 +235,18 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
     const int64_t kfirst =
         s.k0 + (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / G);
     if (kfirst >= s.k1) return;  // whole warps exit together
-    const int64_t k = kfirst + lane / G;
-    const bool live = k < s.k1;  // a tail group past the range still joins the shuffles
+    const int64_t row = kfirst + lane / G;  // table row; the cell itself when not Morton-ordered
+    const bool live = row < s.k1;  // a tail group past the range still joins the shuffles
     const int64_t mend = live ? s.M : 0;
     int cc[D];
-    {
-        int64_t r = k;
+    int64_t k = row;  // lexicographic cell index (keys the draws)
+    if (s.morton) {
+        morton_decode<D>(row, s.mbits, cc);
+        k = 0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) k = k * s.n + cc[l];
+    } else {
+        int64_t r = row;
 #pragma unroll
         for (int l = D - 1; l >= 0; --l) {
             cc[l] = static_cast<int>(r % s.n);
@@ -302,13 +311,13 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
         bool finite = true;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            ytab[k * P + p] = by[p];
+            ytab[row * P + p] = by[p];
             finite = finite && isfinite(by[p]);
         }
         if (!finite) *s.bad = 1;  // NumericError (every step's table, not only the last)
         if constexpr (ANYZ) {
 #pragma unroll
-            for (int j = 0; j < D * P; ++j) ztab[k * D * P + j] = bz[j];
+            for (int j = 0; j < D * P; ++j) ztab[row * D * P + j] = bz[j];
         }
     }
 }
@@ -429,6 +438,34 @@ void launch_step_d(int P, const SrmcDev& s, const double* next, double* y, doubl
         launch_step_t<D, 1>(s, next, y, z, zpass, wantz, st);
     else
         launch_step_t<D, D + 1>(s, next, y, z, zpass, wantz, st);
+}
+
+template <int D>
+__global__ void k_unmorton(int n, int bits, int width, int64_t rows, const double* __restrict__ in,
+                           double* __restrict__ out) {
+    const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= rows) return;
+    int c[D];
+    morton_decode<D>(v, bits, c);
+    int64_t k = 0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) k = k * n + c[l];
+    for (int j = 0; j < width; ++j) out[k * width + j] = in[v * width + j];
+}
+
+cudaError_t launch_unmorton(int d, int n, int bits, int width, const double* in, double* out, cudaStream_t st) {
+    int64_t rows = 1;
+    for (int l = 0; l < d; ++l) rows *= n;
+    const unsigned grid = static_cast<unsigned>((rows + 255) / 256);
+    switch (d) {
+        case 1: k_unmorton<1><<<grid, 256, 0, st>>>(n, bits, width, rows, in, out); break;
+        case 2: k_unmorton<2><<<grid, 256, 0, st>>>(n, bits, width, rows, in, out); break;
+        case 3: k_unmorton<3><<<grid, 256, 0, st>>>(n, bits, width, rows, in, out); break;
+        case 4: k_unmorton<4><<<grid, 256, 0, st>>>(n, bits, width, rows, in, out); break;
+        case 5: k_unmorton<5><<<grid, 256, 0, st>>>(n, bits, width, rows, in, out); break;
+        default: k_unmorton<6><<<grid, 256, 0, st>>>(n, bits, width, rows, in, out); break;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_step(int d, int P, const SrmcDev& s, const double* next, double* y, double* z, bool zpass,

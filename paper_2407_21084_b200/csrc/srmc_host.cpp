@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -132,6 +133,23 @@ std::unique_ptr<qrmc_srmc_plan> make_plan(const qrmc_srmc_problem_t* prob, const
     P->keep_z = keep_z;
     P->anyz = P->zpass || keep_z || cfg->want_z;
     P->base = make_dev(prob, cfg);
+    {
+        // Morton-ordered rows when the grid side is a power of two (srmc_types.h); the
+        // download restores the lexicographic layout. QRMC_SRMC_MORTON=0 keeps row = cell.
+        const int n = cfg->cells_per_dim;
+        const char* e = std::getenv("QRMC_SRMC_MORTON");
+        int bits = 0;
+        while ((1 << bits) < n) ++bits;
+        if (P->d > 1 && n > 1 && (n & (n - 1)) == 0 && bits <= P->d - 1 && P->d * bits <= 30 &&
+            !(e && e[0] == '0')) {
+            P->base.morton = 1;
+            P->base.mbits = bits;
+            for (int b = 0; b < bits; ++b) {
+                P->base.mmul |= 1u << (b * (P->d - 1));
+                P->base.mmask |= 1u << (b * P->d);
+            }
+        }
+    }
     P->cells = P->base.cells;
     P->per = (P->cells + world - 1) / world;
     P->rows = P->per * world;
@@ -214,6 +232,30 @@ void download(qrmc_srmc_plan& P, double* y, size_t y_len, double* z, size_t z_le
     if (z && (!P.dz || z_len < per_y * P.d * P.N))
         fail(QRMC_EINVAL, P.dz ? "z buffer too small (steps * cells * d * P)" : "plan keeps no z tables");
     ck(cudaSetDevice(P.device), "cudaSetDevice");
+    if (P.base.morton) {
+        // back to lexicographic rows through one step-sized scratch table
+        double* tmp = nullptr;
+        ck(cudaMalloc(&tmp, per_y * (z ? P.d : 1) * sizeof(double)), "cudaMalloc download scratch");
+        try {
+            for (int i = 0; i < P.N; ++i) {
+                ck(launch_unmorton(P.d, P.base.n, P.base.mbits, P.P, P.dy + rows_y * i, tmp, P.st), "k_unmorton");
+                ck(cudaMemcpyAsync(y + per_y * i, tmp, per_y * sizeof(double), cudaMemcpyDeviceToHost, P.st), "D2H y");
+                if (z) {
+                    ck(launch_unmorton(P.d, P.base.n, P.base.mbits, P.P * P.d, P.dz + rows_y * P.d * i, tmp, P.st),
+                       "k_unmorton");
+                    ck(cudaMemcpyAsync(z + per_y * P.d * i, tmp, per_y * P.d * sizeof(double), cudaMemcpyDeviceToHost,
+                                       P.st),
+                       "D2H z");
+                }
+            }
+            ck(cudaStreamSynchronize(P.st), "download");
+        } catch (...) {
+            cudaFree(tmp);
+            throw;
+        }
+        cudaFree(tmp);
+        return;
+    }
     for (int i = 0; i < P.N; ++i) {
         ck(cudaMemcpyAsync(y + per_y * i, P.dy + rows_y * i, per_y * sizeof(double), cudaMemcpyDeviceToHost, P.st), "D2H y");
         if (z)

@@ -136,6 +136,8 @@ PARITY_CASES = [
     ("sin-d3-lp1-subwarp", lambda: srmc.sin_bench_problem(3), dict(steps=2, cells_per_dim=33, paths_per_cell=40, basis=srmc.LP1, want_z=True)),
     ("bergman-d3-lp1-subwarp", lambda: _bergman(3, 0.01, 0.06), dict(steps=2, cells_per_dim=33, paths_per_cell=24, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
     ("sin-d6-lp1-one-cell", lambda: srmc.sin_bench_problem(6), dict(steps=3, cells_per_dim=1, paths_per_cell=300, basis=srmc.LP1)),
+    ("sin-d3-lp1-z-morton", lambda: srmc.sin_bench_problem(3), dict(steps=3, cells_per_dim=4, paths_per_cell=40, basis=srmc.LP1, want_z=True)),
+    ("sin-d5-lp1-morton", lambda: srmc.sin_bench_problem(5), dict(steps=2, cells_per_dim=8, paths_per_cell=30, basis=srmc.LP1)),
     ("sin-d4-lp0-trunc", lambda: srmc.sin_bench_problem(4), dict(steps=3, cells_per_dim=4, paths_per_cell=33, basis=srmc.LP0, truncation=1.7)),
     ("bergman-d1-lp1", lambda: _bergman(1, 0.01, 0.06), dict(steps=5, cells_per_dim=32, paths_per_cell=100, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
     ("bergman-d2-lp1", lambda: _bergman(2, 0.01, 0.06), dict(steps=4, cells_per_dim=8, paths_per_cell=96, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
