@@ -127,3 +127,23 @@ def test_gpu_matches_port_live_bases(gpu_lib, port, c):
     assert float(np.abs(coeffs - ref).max()) / scale <= ALPHA_TOL
     assert stats.applications == rs.applications == c["m"] * c["n"] * (c["n"] + 1) // 2
     assert abs(int(stats.clipped) - int(rs.clipped)) <= max(1, rs.clipped // 100000)
+
+
+@pytest.mark.gpu
+def test_gpu_config1_literal_against_reference_build(gpu_lib, port):
+    """BASELINE config 1 as restated in BASELINE.md section 3 at its literal size: d=2,
+    full Gamma_F(31,31) (K=1024), q=0, N=10, M=102,400 -- the reference's own CPU case.
+    Checked against oracle/_ref (the unmodified reference sources) when it travelled
+    with the snapshot, else against the restatement (tools/config1_run.py times it)."""
+    import oracles
+    prob = _abi.sin_bench_problem(2)
+    cfg = _abi.ConfigHolder(steps=10, paths=102_400, damping=0.0, seed=42, gamma_kind=_abi.GAMMA_FULL,
+                            degrees=[31, 31])
+    coeffs, stats, _ = api.backward_solve(prob, cfg)
+    assert coeffs.shape == (10, 1024)
+    R = oracles.ref() if oracles.have_ref() else port
+    ref, rs = R.backward_solve(prob, cfg, 1024)
+    scale = max(1.0, float(np.abs(ref).max()))
+    assert float(np.abs(coeffs - ref).max()) / scale <= ALPHA_TOL
+    assert stats.applications == rs.applications == 102_400 * 10 * 11 // 2
+    assert int(stats.clipped) == int(rs.clipped)
