@@ -1417,8 +1417,12 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                 }
                 // K2 on the tensor cores (QRMC_K2=series forces the series K2)
                 const char* k2 = std::getenv("QRMC_K2");
-                const size_t psmem = project_mma_smem_bytes(off);
-                if (!(k2 && std::strcmp(k2, "series") == 0) && psmem <= static_cast<size_t>(optin) && L.proj_parts > 0) {
+                // QRMC_K2_BATCH=16 forces the narrow batch (tests: both give the same bits)
+                const char* k2b = std::getenv("QRMC_K2_BATCH");
+                int pbatch = project_mma_batch(off, static_cast<size_t>(optin));
+                if (pbatch && k2b && std::atoi(k2b) == kProjBatchNarrow) pbatch = kProjBatchNarrow;
+                const size_t psmem = pbatch ? project_mma_smem_bytes(off, pbatch) : 0;
+                if (!(k2 && std::strcmp(k2, "series") == 0) && pbatch && L.proj_parts > 0) {
                     P->use_proj_mma = true;
                     P->d_pm_rects.alloc(L.proj_rects.size());
                     P->d_pm_rects.upload(L.proj_rects.data(), L.proj_rects.size(), st);
@@ -1437,7 +1441,8 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                         pm.kmax[l] = pa.kmax[l];
                     }
                     pm.basis_size = P->K;
-                    cuda_check(configure_project_mma(d, psmem), "k_project_mma attributes");
+                    pm.batch = pbatch;
+                    cuda_check(configure_project_mma(d, pbatch, psmem), "k_project_mma attributes");
                     P->base.cloud_cos = 1;  // K1 stores cos(pi F(x)) for this K2
                     P->h2d_bytes += L.proj_rects.size() * sizeof(int4) + L.proj_out.size() * sizeof(int32_t);
                 }

@@ -124,7 +124,10 @@ constexpr int kProjWarps = QRMC_PROJ_WARPS;
 #define QRMC_PROJ_TILES 8
 #endif
 constexpr int kProjTiles = QRMC_PROJ_TILES;  // output tiles per warp: ng group blocks x nt term blocks, ng a power of 2
-constexpr int kProjBatch = 16;  // paths per shared-memory table batch (double-buffered)
+// paths per shared-memory table batch (double-buffered): 24 when two tables of
+// 24 + 4 padded columns fit, else 16 (table row strides 28 / 20 doubles; 20 and 28
+// path batches, strides 24 / 32, cost 25-75% more in bank conflicts)
+constexpr int kProjBatchWide = 24, kProjBatchNarrow = 16;
 
 struct ProjMmaArgs {
     const int4* rects;        // [parts][kProjWarps] {gb0, tb0, ng | nt << 8, tiles} (full rectangles)
@@ -137,6 +140,7 @@ struct ProjMmaArgs {
     int offset[kMaxDim];
     int kmax[kMaxDim];
     int64_t basis_size;
+    int batch;                // kProjBatchWide or kProjBatchNarrow (project_mma_batch)
     double* partials;         // [owned_lanes][K]
 };
 
@@ -180,8 +184,10 @@ cudaError_t launch_responses_ws(const StepArgs& a, const WsArgs& m, cudaStream_t
 size_t project_smem_bytes(const ProjArgs& p);
 cudaError_t configure_project(int dim, size_t smem);
 cudaError_t launch_project(const StepArgs& a, const ProjArgs& p, cudaStream_t st);
-size_t project_mma_smem_bytes(int table_len);
-cudaError_t configure_project_mma(int dim, size_t smem);
+size_t project_mma_smem_bytes(int table_len, int batch);
+// the widest batch whose tables fit `optin` bytes, 0 if none
+int project_mma_batch(int table_len, size_t optin);
+cudaError_t configure_project_mma(int dim, int batch, size_t smem);
 cudaError_t launch_project_mma(const StepArgs& a, const ProjMmaArgs& p, cudaStream_t st);
 cudaError_t launch_finish(const StepArgs& a, const FinishArgs& f, cudaStream_t st);
 

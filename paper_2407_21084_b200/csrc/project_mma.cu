@@ -11,7 +11,8 @@
 // as mma.sync.m8n8k4.f64 with M = 8 groups, N = 8 terms, K = 4 paths. Every
 // warp owns one rectangle of ng x nt <= kProjTiles output tiles (host.cpp
 // build_mma_layout) and keeps it in registers while the CTA streams the lane's
-// paths through shared memory in batches of kProjBatch: per batch, the cosine
+// paths through shared memory in batches of B = 24 (16 when the tables of 24 do not
+// fit) paths: per batch, the cosine
 // tables c_k(x_l) of every coordinate are built once ([entry][path] layout as in
 // K1), then each warp forms its W = S * U fragments (per group block) and A
 // fragments (per term block) and issues the DMMAs. The lane's sum over paths is
@@ -30,7 +31,6 @@ namespace qrmc_dev {
 namespace {
 
 constexpr int kThreads = kProjWarps * 32;
-constexpr int kStride = kProjBatch + 4;  // table row stride (paths), padded
 #ifndef QRMC_PROJ_BRANCHLESS
 #define QRMC_PROJ_BRANCHLESS 1
 #endif
@@ -38,38 +38,52 @@ constexpr int kStride = kProjBatch + 4;  // table row stride (paths), padded
 #define QRMC_PROJ_TSPLIT 4
 #endif
 constexpr int kTabSplit = QRMC_PROJ_TSPLIT;
-constexpr int kBatchesPerChunk = kChunk / kProjBatch;
 
-struct ProjSmem {
-    double s[2][kProjBatch];  // S_m of the batch (0 past the chunk's end)
-    // followed by two cosine-table buffers [table_len][kStride]
+// batch geometry: B paths per batch, table row stride B + 4 (paths, padded). A chunk's
+// last batch may be short (B need not divide kChunk): its missing paths read S = 0, so
+// they add exact zeros and the path order of the tensor-core sum is the same for every B.
+template <int B>
+struct BatchGeom {
+    static constexpr int kStride = B + 4;
+    static constexpr int kPerChunk = (kChunk + B - 1) / B;
 };
 
-// batch b of the lane: chunk r = b / kBatchesPerChunk, paths [base, base + n)
+template <int B>
+struct ProjSmem {
+    double s[2][B];  // S_m of the batch (0 past the chunk's end)
+    // followed by two cosine-table buffers [table_len][B + 4]
+};
+
+// batch b of the lane: chunk r = b / kPerChunk, paths [base, base + n)
 struct Batch {
     int64_t q0, m0;  // owned index and path number of the first path
     int n;           // paths (<= 0: past the lane's end)
 };
 
+template <int B>
 __device__ __forceinline__ Batch lane_batch(const StepArgs& a, int lane_rel, int b) {
-    const int64_t r = b / kBatchesPerChunk;
-    const int base = (b % kBatchesPerChunk) * kProjBatch;
+    constexpr int kPerChunk = BatchGeom<B>::kPerChunk;
+    const int64_t r = b / kPerChunk;
+    const int base = (b % kPerChunk) * B;
     const int64_t c = static_cast<int64_t>(a.lane_lo + lane_rel) + r * kLanes;
     Batch bt;
     bt.q0 = (r * a.owned_lanes + lane_rel) * kChunk + base;
     bt.m0 = c * kChunk + base;
-    const int64_t rem = a.paths - bt.m0;
-    bt.n = static_cast<int>(rem < kProjBatch ? (rem < 0 ? 0 : rem) : kProjBatch);
+    int64_t rem = a.paths - bt.m0;
+    if (rem > kChunk - base) rem = kChunk - base;
+    bt.n = static_cast<int>(rem < B ? (rem < 0 ? 0 : rem) : B);
     return bt;
 }
 
 }  // namespace
 
 // The batch loop of one warp shape: NG group blocks x up to 8 / NG term blocks.
-template <int D, int NG, bool GEN>
-__device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArgs& p, ProjSmem& sm, double* tabs0,
+template <int D, int NG, bool GEN, int B>
+__device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArgs& p, ProjSmem<B>& sm, double* tabs0,
                                              size_t tab_elems, int lane_rel, int slot, int4 rc) {
     constexpr int NT = kProjTiles / NG;
+    constexpr int kStride = BatchGeom<B>::kStride;
+    constexpr int kProjBatch = B;
     const int tid = threadIdx.x, lane = tid & 31;
     const int gb0 = rc.x, tb0 = rc.y, nt = rc.z >> 8;
     const int row = lane >> 2, col = lane & 3;
@@ -99,14 +113,14 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
     const int pt = tid % kProjBatch, tq = (tid / kProjBatch) % TS, tl = tid / (kProjBatch * TS);
     const int64_t chunks_total = (a.paths + kChunk - 1) / kChunk;
     const int64_t my_chunks = (chunks_total - (a.lane_lo + lane_rel) + kLanes - 1) / kLanes;
-    const int n_batches = static_cast<int>(my_chunks) * kBatchesPerChunk;
+    const int n_batches = static_cast<int>(my_chunks) * BatchGeom<B>::kPerChunk;
     // cos theta_l (and S) of this thread's task in batch b, fetched a batch ahead
     auto fetch = [&](int b, double& c1, double& sv) {
         c1 = 1.0;
         sv = 0.0;
         if (b >= n_batches || tid >= kTasks) return;
         {
-            const Batch bt = lane_batch(a, lane_rel, b);
+            const Batch bt = lane_batch<B>(a, lane_rel, b);
             if (pt >= bt.n) return;
             if (a.cloud && a.cloud_cos) {
                 c1 = a.cloud[tl * a.n_owned + bt.q0 + pt];
@@ -198,15 +212,15 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
             }
 }
 
-template <int D, bool GEN>
+template <int D, bool GEN, int B>
 __global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, const ProjMmaArgs p) {
     static_assert(D >= 3, "the tensor-core K2 needs an upper prefix");
-    static_assert(kProjBatch % 4 == 0 && kChunk % kProjBatch == 0, "batches of whole k-steps inside chunks");
-    static_assert(kProjBatch * D <= kThreads, "one table task per thread");
+    static_assert(B % 4 == 0 && kChunk % 4 == 0, "batches of whole k-steps inside chunks");
+    static_assert(B * D <= kThreads, "one table task per thread");
     extern __shared__ __align__(16) unsigned char dsm[];
-    ProjSmem& sm = *reinterpret_cast<ProjSmem*>(dsm);
-    double* tabs0 = reinterpret_cast<double*>(dsm + ((sizeof(ProjSmem) + 15) & ~size_t{15}));
-    const size_t tab_elems = static_cast<size_t>(p.table_len) * kStride;
+    ProjSmem<B>& sm = *reinterpret_cast<ProjSmem<B>*>(dsm);
+    double* tabs0 = reinterpret_cast<double*>(dsm + ((sizeof(ProjSmem<B>) + 15) & ~size_t{15}));
+    const size_t tab_elems = static_cast<size_t>(p.table_len) * BatchGeom<B>::kStride;
     const int warp = threadIdx.x >> 5;
     const int part = blockIdx.x, lane_rel = blockIdx.y;
     const int slot = part * kProjWarps + warp;
@@ -215,51 +229,69 @@ __global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, c
     // sets its register tile. Empty slots carry tiles = 0 and write nothing.
     switch (rc.z & 0xFF) {
         case 16:
-            if constexpr (kProjTiles >= 16) project_rect<D, 16, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 16) project_rect<D, 16, GEN, B>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
         case 8:
-            if constexpr (kProjTiles >= 8) project_rect<D, 8, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 8) project_rect<D, 8, GEN, B>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
         case 4:
-            if constexpr (kProjTiles >= 4) project_rect<D, 4, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 4) project_rect<D, 4, GEN, B>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
         case 2:
-            if constexpr (kProjTiles >= 2) project_rect<D, 2, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
+            if constexpr (kProjTiles >= 2) project_rect<D, 2, GEN, B>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
             break;
-        default: project_rect<D, 1, GEN>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
+        default: project_rect<D, 1, GEN, B>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc); break;
     }
 }
 
-size_t project_mma_smem_bytes(int table_len) {
-    return ((sizeof(ProjSmem) + 15) & ~size_t{15}) + 2 * static_cast<size_t>(kStride) * table_len * sizeof(double);
+template <int B>
+static size_t smem_bytes_b(int table_len) {
+    return ((sizeof(ProjSmem<B>) + 15) & ~size_t{15}) +
+           2 * static_cast<size_t>(BatchGeom<B>::kStride) * table_len * sizeof(double);
+}
+
+size_t project_mma_smem_bytes(int table_len, int batch) {
+    return batch == kProjBatchWide ? smem_bytes_b<kProjBatchWide>(table_len) : smem_bytes_b<kProjBatchNarrow>(table_len);
+}
+
+int project_mma_batch(int table_len, size_t optin) {
+    if (smem_bytes_b<kProjBatchWide>(table_len) <= optin) return kProjBatchWide;
+    if (smem_bytes_b<kProjBatchNarrow>(table_len) <= optin) return kProjBatchNarrow;
+    return 0;
+}
+
+template <int D, int B, class Fn>
+static cudaError_t with_project_kernel_b(bool gen, Fn&& fn) {
+    return gen ? fn(k_project_mma<D, true, B>) : fn(k_project_mma<D, false, B>);
 }
 
 template <class Fn>
-static cudaError_t with_project_kernel(int dim, bool gen, Fn&& fn) {
+static cudaError_t with_project_kernel(int dim, int batch, bool gen, Fn&& fn) {
+    const bool wide = batch == kProjBatchWide;
     switch (dim) {
-        case 3: return gen ? fn(k_project_mma<3, true>) : fn(k_project_mma<3, false>);
-        case 4: return gen ? fn(k_project_mma<4, true>) : fn(k_project_mma<4, false>);
-        case 5: return gen ? fn(k_project_mma<5, true>) : fn(k_project_mma<5, false>);
-        case 6: return gen ? fn(k_project_mma<6, true>) : fn(k_project_mma<6, false>);
-        case 7: return gen ? fn(k_project_mma<7, true>) : fn(k_project_mma<7, false>);
-        case 8: return gen ? fn(k_project_mma<8, true>) : fn(k_project_mma<8, false>);
+        case 3: return wide ? with_project_kernel_b<3, kProjBatchWide>(gen, fn) : with_project_kernel_b<3, kProjBatchNarrow>(gen, fn);
+        case 4: return wide ? with_project_kernel_b<4, kProjBatchWide>(gen, fn) : with_project_kernel_b<4, kProjBatchNarrow>(gen, fn);
+        case 5: return wide ? with_project_kernel_b<5, kProjBatchWide>(gen, fn) : with_project_kernel_b<5, kProjBatchNarrow>(gen, fn);
+        case 6: return wide ? with_project_kernel_b<6, kProjBatchWide>(gen, fn) : with_project_kernel_b<6, kProjBatchNarrow>(gen, fn);
+        case 7: return wide ? with_project_kernel_b<7, kProjBatchWide>(gen, fn) : with_project_kernel_b<7, kProjBatchNarrow>(gen, fn);
+        case 8: return wide ? with_project_kernel_b<8, kProjBatchWide>(gen, fn) : with_project_kernel_b<8, kProjBatchNarrow>(gen, fn);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t configure_project_mma(int dim, size_t smem) {
+cudaError_t configure_project_mma(int dim, int batch, size_t smem) {
     auto set = [&](auto kern) {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     };
-    const cudaError_t e = with_project_kernel(dim, false, set);
-    return e != cudaSuccess ? e : with_project_kernel(dim, true, set);
+    const cudaError_t e = with_project_kernel(dim, batch, false, set);
+    return e != cudaSuccess ? e : with_project_kernel(dim, batch, true, set);
 }
 
 cudaError_t launch_project_mma(const StepArgs& a, const ProjMmaArgs& p, cudaStream_t st) {
     if (a.owned_lanes == 0 || p.parts == 0) return cudaSuccess;
     const dim3 grid(static_cast<unsigned>(p.parts), static_cast<unsigned>(a.owned_lanes));
-    return with_project_kernel(a.prob.dim, a.meas.form == 3, [&](auto kern) {
-        kern<<<grid, kThreads, project_mma_smem_bytes(p.table_len), st>>>(a, p);
+    return with_project_kernel(a.prob.dim, p.batch, a.meas.form == 3, [&](auto kern) {
+        kern<<<grid, kThreads, project_mma_smem_bytes(p.table_len, p.batch), st>>>(a, p);
         return cudaGetLastError();
     });
 }

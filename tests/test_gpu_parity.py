@@ -292,6 +292,21 @@ def test_ring_tensor_core_k1_matches_reference(L, entry, monkeypatch):
     assert (stats.applications, stats.clipped) == (entry["applications"], entry["clipped"])
 
 
+@pytest.mark.parametrize("dim,deg,paths", [(3, 8, 5000), (4, 100, 3000), (6, 16, 2051)])
+def test_k2_batch_width_does_not_change_bits(L, monkeypatch, dim, deg, paths):
+    # K2 stages 24 paths per shared-memory batch (16 when those tables do not fit);
+    # a chunk's short last batch adds exact zeros, so the tensor-core sum over paths
+    # runs in the same order either way and the coefficients agree bit for bit
+    prob = _abi.sin_bench_problem(dim)
+    cfg = _abi.ConfigHolder(steps=3, paths=paths, damping=5.1, seed=5, gamma_kind=2, degrees=[deg])
+    wide, sw, _ = api.backward_solve(prob, cfg)
+    monkeypatch.setenv("QRMC_K2_BATCH", "16")
+    assert _kernel_names(prob, cfg)[1] == "k_project_mma"
+    narrow, sn, _ = api.backward_solve(prob, cfg)
+    np.testing.assert_array_equal(wide, narrow)
+    assert (sw.applications, sw.clipped) == (sn.applications, sn.clipped)
+
+
 @pytest.mark.parametrize("dim,deg", [(5, 12), (6, 8)])
 def test_forced_ws_k1_matches_port_for_more_coordinates(L, port, monkeypatch, dim, deg):
     # the warp-specialised K1 stays correct where the plan prefers k_responses_mma
