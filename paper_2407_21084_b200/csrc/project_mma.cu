@@ -213,7 +213,10 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
 }
 
 template <int D, bool GEN, int B>
-__global__ void __launch_bounds__(kThreads, 1) k_project_mma(const StepArgs a, const ProjMmaArgs p) {
+#ifndef QRMC_PROJ_MINB
+#define QRMC_PROJ_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, QRMC_PROJ_MINB) k_project_mma(const StepArgs a, const ProjMmaArgs p) {
     static_assert(D >= 3, "the tensor-core K2 needs an upper prefix");
     static_assert(B % 4 == 0 && kChunk % 4 == 0, "batches of whole k-steps inside chunks");
     static_assert(B * D <= kThreads, "one table task per thread");
