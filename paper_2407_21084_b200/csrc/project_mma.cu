@@ -39,6 +39,14 @@ constexpr int kThreads = kProjWarps * 32;
 #endif
 constexpr int kTabSplit = QRMC_PROJ_TSPLIT;
 
+// The batch loop's CTA barrier. Warps of one CTA run different project_rect shape
+// instantiations, so they reach it from different code locations: a named barrier
+// (id 1, all kThreads threads) is defined by its id and arrival count, which PTX
+// specifies for exactly this case (unlike __syncthreads in divergent call sites).
+__device__ __forceinline__ void batch_barrier() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+}
+
 // batch geometry: B paths per batch, table row stride B + 4 (paths, padded). A chunk's
 // last batch may be short (B need not divide kChunk): its missing paths read S = 0, so
 // they add exact zeros and the path order of the tensor-core sum is the same for every B.
@@ -150,7 +158,7 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
     fetch(0, cn, sn);
     build(0, cn, sn);
     fetch(1, cn, sn);
-    __syncthreads();
+    batch_barrier();
     for (int b = 0; b < n_batches; ++b) {
         const int buf = b & 1;
         // tables of batch b+1 (other buffer) while the tensor cores take batch b
@@ -194,7 +202,7 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
             }
 #endif
         }
-        __syncthreads();
+        batch_barrier();
     }
     // partial[lane][k] = sqrt2^{nnz(k)} G[u][t]
     double* out = p.partials + static_cast<int64_t>(lane_rel) * p.basis_size;
@@ -228,8 +236,8 @@ __global__ void __launch_bounds__(kThreads, QRMC_PROJ_MINB) k_project_mma(const 
     const int part = blockIdx.x, lane_rel = blockIdx.y;
     const int slot = part * kProjWarps + warp;
     const int4 rc = __ldg(&p.rects[slot]);
-    // every warp runs the same batch loop (barriers included); the shape only
-    // sets its register tile. Empty slots carry tiles = 0 and write nothing.
+    // every warp runs the same batch loop (named barrier batch_barrier); the shape
+    // only sets its register tile. Empty slots carry tiles = 0 and write nothing.
     switch (rc.z & 0xFF) {
         case 16:
             if constexpr (kProjTiles >= 16) project_rect<D, 16, GEN, B>(a, p, sm, tabs0, tab_elems, lane_rel, slot, rc);
