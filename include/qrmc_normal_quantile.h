@@ -135,6 +135,42 @@ QRMC_HD double qrmc_ppnd16(double p) {
     return q < 0 ? -val : val;
 }
 
+/* qrmc_ppnd16's two branches on their own (the same operations, so the same results):
+ * the central region |p - 1/2| <= 0.425 from q = p - 1/2, and the tails from
+ * r = (q < 0 ? p : 1 - p), returning the magnitude (the caller applies the sign of q).
+ * Kernels that batch the rare tail evaluations across a warp use these. */
+QRMC_HD double qrmc_ppnd16_central(double q) {
+    const double r = QRMC_SUB(0.180625, QRMC_MUL(q, q));
+    double num = QRMC_NQC(0), den = QRMC_NQC(8);
+    num = QRMC_HSTEP(num, r, QRMC_NQC(1));
+    num = QRMC_HSTEP(num, r, QRMC_NQC(2));
+    num = QRMC_HSTEP(num, r, QRMC_NQC(3));
+    num = QRMC_HSTEP(num, r, QRMC_NQC(4));
+    num = QRMC_HSTEP(num, r, QRMC_NQC(5));
+    num = QRMC_HSTEP(num, r, QRMC_NQC(6));
+    num = QRMC_HSTEP(num, r, QRMC_NQC(7));
+    den = QRMC_HSTEP(den, r, QRMC_NQC(9));
+    den = QRMC_HSTEP(den, r, QRMC_NQC(10));
+    den = QRMC_HSTEP(den, r, QRMC_NQC(11));
+    den = QRMC_HSTEP(den, r, QRMC_NQC(12));
+    den = QRMC_HSTEP(den, r, QRMC_NQC(13));
+    den = QRMC_HSTEP(den, r, QRMC_NQC(14));
+    den = QRMC_HSTEP(den, r, QRMC_NQC(15));
+    return QRMC_DIV(QRMC_MUL(q, num), den);
+}
+
+QRMC_HD double qrmc_ppnd16_tail(double r) {
+    r = QRMC_SQRT(-QRMC_LOG(r));
+    const int c = r <= 5.0 ? 16 : 32;
+    r = QRMC_SUB(r, c == 16 ? 1.6 : 5.0);
+    double num = QRMC_NQC(c), den = QRMC_NQC(c + 8);
+    for (int j = 1; j < 8; ++j) {
+        num = QRMC_HSTEP(num, r, QRMC_NQC(c + j));
+        den = QRMC_HSTEP(den, r, QRMC_NQC(c + 8 + j));
+    }
+    return QRMC_DIV(num, den);
+}
+
 /* Boost-shaped erfc^{-1}(z), z in (0, 2). */
 QRMC_HD double qrmc_erfc_inv(double z) {
     return QRMC_DIV(-qrmc_ppnd16(QRMC_MUL(0.5, z)), QRMC_ROOT_TWO);

@@ -247,3 +247,18 @@ double srmc_oracle_eval(const qrmc_srmc_problem_t* prob, const qrmc_srmc_config_
     s.inv2h = 2.0 / s.h;
     return s_eval(&s, y_step, x);
 }
+
+/* PPND16 of n uniforms two ways, for the header check (tests/test_srmc.py): whole, and
+ * through the split branches the device batches across a warp (srmc.cu srmc_quantiles). */
+void srmc_oracle_ppnd16_both(const double* u, int64_t n, double* whole, double* split) {
+    for (int64_t i = 0; i < n; ++i) {
+        const double q = u[i] - 0.5;
+        whole[i] = qrmc_ppnd16(u[i]);
+        if ((q < 0 ? -q : q) <= 0.425) {
+            split[i] = qrmc_ppnd16_central(q);
+        } else {
+            const double v = qrmc_ppnd16_tail(q < 0 ? u[i] : 1.0 - u[i]);
+            split[i] = q < 0 ? -v : v;
+        }
+    }
+}

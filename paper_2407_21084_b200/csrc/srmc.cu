@@ -164,17 +164,69 @@ __device__ __forceinline__ void chol_solve(const double* A, double* b) {
 // reference path; SRMC's draws are its own (oracle/srmc_oracle.c does the same).
 __device__ __noinline__ double srmc_normal_quantile(double u) { return qrmc_ppnd16(u); }
 
+// PPND16 for the D Gaussian increments of one path per lane, the tails batched over the
+// warp. About 15% of uniforms fall in the tails (|u - 1/2| > 0.425), so nearly every warp
+// of 32 lanes holds one and, evaluated per lane, every quantile would cost the warp the
+// central rational AND the tail's log, sqrt and rational. Here each lane evaluates its D
+// central rationals, then the warp's tail arguments (ballot prefix over the lanes) are
+// dealt out one per lane through shared memory and evaluated in ceil(tails / 32) rounds.
+// Every value goes through the same operations as qrmc_ppnd16 (bit-identical).
+// All 32 lanes must call it together (the kernel runs uniform trip counts).
+__device__ __noinline__ double srmc_central(double q) { return qrmc_ppnd16_central(q); }
+__device__ __noinline__ double srmc_tail(double r) { return qrmc_ppnd16_tail(r); }
+
+template <int D>
+__device__ __forceinline__ void srmc_quantiles(double* uz, double* scratch) {
+    // uz: the D uniforms in, the D normals out (in place, to keep registers down)
+    static_assert(D <= 7, "tail counts are gathered in three ballot bits");
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned tails = 0, neg = 0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        const double q = DSUB(uz[l], 0.5);
+        if ((q < 0 ? -q : q) > 0.425) tails |= 1u << l;
+        if (q < 0) neg |= 1u << l;
+    }
+    const int cnt = __popc(tails);
+    const unsigned b0 = __ballot_sync(0xffffffffu, cnt & 1), b1 = __ballot_sync(0xffffffffu, cnt & 2),
+                   b2 = __ballot_sync(0xffffffffu, cnt & 4);
+    const int total = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+    const int excl = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+    if (total) {  // warp-uniform
+        int o = excl;
+#pragma unroll
+        for (int l = 0; l < D; ++l)
+            if ((tails >> l) & 1u) scratch[o++] = (neg >> l) & 1u ? uz[l] : DSUB(1.0, uz[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < D; ++l) uz[l] = srmc_central(DSUB(uz[l], 0.5));
+    if (total == 0) return;
+    __syncwarp();
+    for (int g = lane; g < total; g += 32) scratch[g] = srmc_tail(scratch[g]);
+    __syncwarp();
+    {
+        int o = excl;
+#pragma unroll
+        for (int l = 0; l < D; ++l)
+            if ((tails >> l) & 1u) {
+                const double v = scratch[o++];
+                uz[l] = (neg >> l) & 1u ? -v : v;
+            }
+    }
+    __syncwarp();  // the scratch is reused by the next path
+}
+
 // One path of cell k: start X_i (and its local coordinates), dW, endpoint response Y1.
 template <int D, int P>
 __device__ __forceinline__ void srmc_path(const SrmcDev& s, const double* __restrict__ next, const int* cc,
-                                          int64_t k, int64_t m, double* x0, double* sl, double* dw, double* x1, double& y1) {
+                                          int64_t k, int64_t m, double* x0, double* sl, double* dw, double* x1, double& y1,
+                                          double* scratch) {
     // The path's 2D draws are blocks 0..D-1 of its stream (draw n = half n&1 of block n>>1,
     // rng.hpp:26-65): uniforms 0..D-1 place the start, D..2D-1 are the Gaussian increments.
     // Round keys come precomputed from the launch parameters (no per-thread key schedule).
     const uint64_t sid = sid_training(s.step, static_cast<uint64_t>(k) * static_cast<uint64_t>(s.M) + m);
-    uint64_t w[2 * D];
-#pragma unroll
-    for (int b = 0; b < D; ++b) {
+    auto block = [&](int b) {
         uint4 c = make_uint4(static_cast<uint32_t>(b), 0u, static_cast<uint32_t>(sid), static_cast<uint32_t>(sid >> 32));
 #pragma unroll
         for (int r = 0; r < 10; ++r) {
@@ -182,19 +234,39 @@ __device__ __forceinline__ void srmc_path(const SrmcDev& s, const double* __rest
             const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
             c = make_uint4(hi1 ^ c.y ^ s.rk[2 * r], lo1, hi0 ^ c.w ^ s.rk[2 * r + 1], lo0);
         }
-        w[2 * b] = (static_cast<uint64_t>(c.y) << 32) | c.x;
-        w[2 * b + 1] = (static_cast<uint64_t>(c.w) << 32) | c.z;
+        return c;
+    };
+    auto uni = [](uint32_t lo, uint32_t hi) {
+        const uint64_t x = (static_cast<uint64_t>(hi) << 32) | lo;
+        return DMUL(DADD(static_cast<double>(x >> 12), 0.5), 0x1p-52);
+    };
+    // the Gaussian increments first (draws D..2D-1, so the words die before the start is
+    // drawn), then the start (draws 0..D-1); with D odd, block D/2 holds one of each
+    double uz[D];
+    uint4 shared_block = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int b = D / 2; b < D; ++b) {
+        const uint4 c = block(b);
+        if (2 * b >= D) uz[2 * b - D] = uni(c.x, c.y);
+        else shared_block = c;
+        if (2 * b + 1 < 2 * D) uz[2 * b + 1 - D] = uni(c.z, c.w);
+    }
+    srmc_quantiles<D>(uz, scratch);
+#pragma unroll
+    for (int b = 0; b < (D + 1) / 2; ++b) {
+        const uint4 c = (D % 2 == 1 && b == D / 2) ? shared_block : block(b);
+        const double u0 = uni(c.x, c.y);
+        x0[2 * b] = DADD(s.lo, DMUL(DADD(static_cast<double>(cc[2 * b]), u0), s.h));
+        sl[2 * b] = DSUB(DMUL(2.0, u0), 1.0);
+        if (2 * b + 1 < D) {
+            const double u1 = uni(c.z, c.w);
+            x0[2 * b + 1] = DADD(s.lo, DMUL(DADD(static_cast<double>(cc[2 * b + 1]), u1), s.h));
+            sl[2 * b + 1] = DSUB(DMUL(2.0, u1), 1.0);
+        }
     }
 #pragma unroll
     for (int l = 0; l < D; ++l) {
-        const double u = DMUL(DADD(static_cast<double>(w[l] >> 12), 0.5), 0x1p-52);
-        x0[l] = DADD(s.lo, DMUL(DADD(static_cast<double>(cc[l]), u), s.h));
-        sl[l] = DSUB(DMUL(2.0, u), 1.0);
-    }
-#pragma unroll
-    for (int l = 0; l < D; ++l) {
-        const double u = DMUL(DADD(static_cast<double>(w[D + l] >> 12), 0.5), 0x1p-52);
-        dw[l] = DMUL(s.sqrt_dt, srmc_normal_quantile(u));
+        dw[l] = DMUL(s.sqrt_dt, uz[l]);
         x1[l] = DADD(DADD(x0[l], s.bdt), DMUL(s.sig, dw[l]));
     }
     if (s.last) {
@@ -263,10 +335,18 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
 #pragma unroll
     for (int j = 0; j < (ANYZ ? D * P : 1); ++j) bz[j] = 0.0;
 
+    // every lane runs the warp's trip count (srmc_quantiles is warp-collective); a lane's
+    // iterations past its own paths (m >= mend) accumulate nothing, so each lane still sums
+    // exactly its paths sub, sub + G, ... in order
+    __shared__ double tail_scratch[8][32 * D];  // 8 warps per block (launch_step_t)
+    double* scratch = tail_scratch[threadIdx.x >> 5];
+    const int64_t iters = (s.M + G - 1) / G;
     double x0[D], sl[D], dw[D], x1[D], phi[P], y1;
     const double zero_z[D] = {};
-    for (int64_t m = sub; m < mend; m += G) {
-        srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1);
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t m = sub + it * G;
+        srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1, scratch);
+        if (m >= mend) continue;
         phi_of<D, P>(sl, phi);
         acc_gram<D, P>(A, phi);
         if constexpr (ANYZ) {
@@ -289,8 +369,10 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
         chol_solve<P, D>(A, bz);
     }
     if constexpr (ZPASS) {
-        for (int64_t m = sub; m < mend; m += G) {
-            srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1);
+        for (int64_t it = 0; it < iters; ++it) {
+            const int64_t m = sub + it * G;
+            srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1, scratch);
+            if (m >= mend) continue;
             phi_of<D, P>(sl, phi);
             double zi[D];
 #pragma unroll

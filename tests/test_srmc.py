@@ -276,3 +276,21 @@ def test_plan_reports_non_finite_tables():
     with pytest.raises(srmc.SrmcError) as e:
         srmc.solve(p, srmc.config(3, 4, 64))
     assert e.value.code == 2
+
+
+def test_ppnd16_split_branches_equal_the_whole():
+    """The device evaluates PPND16's central rational per lane and batches the tails over
+    the warp (srmc.cu srmc_quantiles) through qrmc_ppnd16_central / qrmc_ppnd16_tail;
+    the two branches must reproduce qrmc_ppnd16 bit for bit (include/qrmc_normal_quantile.h)."""
+    import ctypes as C
+    o = oracles.srmc_port()
+    f = o.L.srmc_oracle_ppnd16_both
+    dp = C.POINTER(C.c_double)
+    f.argtypes = [dp, C.c_int64, dp, dp]
+    rng = np.random.default_rng(3)
+    u = np.concatenate([rng.random(200_000), [0.075, 0.925, 0.5 - 0.425, 0.5 + 0.425, 1e-300, 1e-16, 1 - 2**-53,
+                                              np.nextafter(0.075, 0), np.nextafter(0.925, 1), 2.0**-1074]])
+    u = np.concatenate([u, np.exp(-rng.random(5000) * 700)])  # deep tails (r > 5 branch)
+    whole, split = np.zeros_like(u), np.zeros_like(u)
+    f(u.ctypes.data_as(dp), u.size, whole.ctypes.data_as(dp), split.ctypes.data_as(dp))
+    np.testing.assert_array_equal(whole, split)
