@@ -156,13 +156,12 @@ __device__ __forceinline__ void chol_solve(const double* A, double* b) {
     }
 }
 
-// The quantile is called 2-pass x D times per path; one out-of-line copy keeps the
-// kernel's instruction footprint small (bit-identical arithmetic).
 // SRMC's Gaussian increments are PPND16(u) itself (AS241, include/qrmc_normal_quantile.h):
 // the reference's composition -sqrt(2) * erfc_inv(2u) = -sqrt(2) * (-PPND16(u) / sqrt(2))
 // adds a division and a multiplication that only matter for bit parity with the GQRMDP
-// reference path; SRMC's draws are its own (oracle/srmc_oracle.c does the same).
-__device__ __noinline__ double srmc_normal_quantile(double u) { return qrmc_ppnd16(u); }
+// reference path; SRMC's draws are its own (oracle/srmc_oracle.c does the same). The tail
+// branch is one out-of-line copy, which keeps the kernel's instruction footprint small;
+// the short central rational is inlined (4% faster than an out-of-line call).
 
 // PPND16 for the D Gaussian increments of one path per lane, the tails batched over the
 // warp. About 15% of uniforms fall in the tails (|u - 1/2| > 0.425), so nearly every warp
@@ -172,7 +171,7 @@ __device__ __noinline__ double srmc_normal_quantile(double u) { return qrmc_ppnd
 // dealt out one per lane through shared memory and evaluated in ceil(tails / 32) rounds.
 // Every value goes through the same operations as qrmc_ppnd16 (bit-identical).
 // All 32 lanes must call it together (the kernel runs uniform trip counts).
-__device__ __noinline__ double srmc_central(double q) { return qrmc_ppnd16_central(q); }
+__device__ __forceinline__ double srmc_central(double q) { return qrmc_ppnd16_central(q); }
 __device__ __noinline__ double srmc_tail(double r) { return qrmc_ppnd16_tail(r); }
 
 template <int D>
@@ -490,17 +489,22 @@ template <int D, int P>
 void launch_step_t(const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz, cudaStream_t st) {
     const int warps = 8;
     const int64_t cells = s.k1 - s.k0;
-    // 8 lanes per hypercube, 4 hypercubes per warp -- only when the range still fills the
-    // GPU with quarter as many warps (64^2 cells at M=100: 1.33e10 -> 1.1e10 otherwise)
+    // 4 lanes per hypercube, 8 hypercubes per warp -- only when the range still fills the
+    // GPU with an eighth as many warps (64^2 cells at M=100: 1.33e10 -> 1.1e10 with a warp
+    // per cell; config 4: 4 lanes 1.92e10, 8 lanes 1.83e10, 2 / 1 lanes +0.5 / +1%)
     if (s.M < 256 && s.cells >= 32768) {  // by the TOTAL cell count: a shard computes exactly what the whole solve does
-        const unsigned grid = static_cast<unsigned>((cells + warps * 4 - 1) / (warps * 4));
+#ifndef QRMC_SRMC_SUBG
+#define QRMC_SRMC_SUBG 4
+#endif
+        constexpr int SG = QRMC_SRMC_SUBG, CPW = 32 / SG;  // lanes per hypercube, hypercubes per warp
+        const unsigned grid = static_cast<unsigned>((cells + warps * CPW - 1) / (warps * CPW));
         if (grid == 0) return;
         if (zpass)
-            k_srmc_step<D, P, true, false, 8><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+            k_srmc_step<D, P, true, false, SG><<<grid, warps * 32, 0, st>>>(s, next, y, z);
         else if (wantz)
-            k_srmc_step<D, P, false, true, 8><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+            k_srmc_step<D, P, false, true, SG><<<grid, warps * 32, 0, st>>>(s, next, y, z);
         else
-            k_srmc_step<D, P, false, false, 8><<<grid, warps * 32, 0, st>>>(s, next, y, z);
+            k_srmc_step<D, P, false, false, SG><<<grid, warps * 32, 0, st>>>(s, next, y, z);
         return;
     }
     const unsigned grid = static_cast<unsigned>((cells + warps - 1) / warps);

@@ -132,7 +132,7 @@ PARITY_CASES = [
     ("sin-d1-lp0", lambda: srmc.sin_bench_problem(1), dict(steps=5, cells_per_dim=16, paths_per_cell=45, basis=srmc.LP0)),
     ("sin-d2-lp1-z", lambda: srmc.sin_bench_problem(2), dict(steps=4, cells_per_dim=8, paths_per_cell=64, basis=srmc.LP1, want_z=True)),
     ("sin-d3-lp1", lambda: srmc.sin_bench_problem(3), dict(steps=3, cells_per_dim=5, paths_per_cell=37, basis=srmc.LP1)),
-    # >= 32768 cells and M < 256: 8 lanes per hypercube (4 per warp), 33^3 leaves a tail group
+    # >= 32768 cells and M < 256: 4 lanes per hypercube (8 per warp), 33^3 leaves a tail group
     ("sin-d3-lp1-subwarp", lambda: srmc.sin_bench_problem(3), dict(steps=2, cells_per_dim=33, paths_per_cell=40, basis=srmc.LP1, want_z=True)),
     ("bergman-d3-lp1-subwarp", lambda: _bergman(3, 0.01, 0.06), dict(steps=2, cells_per_dim=33, paths_per_cell=24, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
     ("sin-d6-lp1-one-cell", lambda: srmc.sin_bench_problem(6), dict(steps=3, cells_per_dim=1, paths_per_cell=300, basis=srmc.LP1)),
