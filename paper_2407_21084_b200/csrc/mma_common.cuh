@@ -32,8 +32,11 @@ __device__ __forceinline__ uint64_t stream_u64_at(uint64_t seed, uint64_t sid, u
         make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)));
     return (idx & 1) ? ((static_cast<uint64_t>(o.w) << 32) | o.z) : ((static_cast<uint64_t>(o.y) << 32) | o.x);
 }
+// ((v >> 12) + 1/2) 2^-52 (rng.hpp:41-43) without an integer->double conversion: m = v >> 12
+// in the mantissa of 1.0 gives 1 + m 2^-52; minus 1 and plus 2^-53 are exact ((2m + 1) 2^-53
+// has 53 significant bits), so this is the same double
 __device__ __forceinline__ double u64_to_uniform(uint64_t v) {
-    return DMUL(DADD(static_cast<double>(v >> 12), 0.5), 0x1p-52);
+    return DADD(DSUB(__longlong_as_double(static_cast<long long>(0x3FF0000000000000ull | (v >> 12))), 1.0), 0x1p-53);
 }
 
 __device__ __forceinline__ int64_t owned_path(const StepArgs& a, int64_t q) {

@@ -73,9 +73,12 @@ struct Stream {
         pos = 1;
         return (static_cast<uint64_t>(o.y) << 32) | o.x;
     }
-    // ((x >> 12) + 0.5) * 2^-52 (rng.hpp:41-43): exact in binary64.
+    // ((x >> 12) + 0.5) * 2^-52 (rng.hpp:41-43): exact in binary64, formed without an
+    // integer->double conversion (m = x >> 12 in the mantissa of 1.0, minus 1, plus 2^-53;
+    // every step exact, so the same double)
     __device__ __forceinline__ double next_uniform() {
-        return DMUL(DADD(static_cast<double>(next_u64() >> 12), 0.5), 0x1p-52);
+        const uint64_t m = next_u64() >> 12;
+        return DADD(DSUB(__longlong_as_double(static_cast<long long>(0x3FF0000000000000ull | m)), 1.0), 0x1p-53);
     }
     // normal_quantile(next_uniform()) (rng.cpp:42-49)
     __device__ __forceinline__ double next_normal() { return qrmc_normal_quantile(next_uniform()); }

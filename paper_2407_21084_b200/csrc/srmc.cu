@@ -235,6 +235,9 @@ __device__ __forceinline__ void srmc_path(const SrmcDev& s, const double* __rest
         }
         return c;
     };
+    // u = ((x >> 12) + 1/2) 2^-52 (rng.hpp:41-43). (The conversion-free form K1 uses,
+    // mma_common.cuh u64_to_uniform, is 1% slower here: this kernel is FP64-pipe bound and
+    // the integer->double conversion is not on that pipe.)
     auto uni = [](uint32_t lo, uint32_t hi) {
         const uint64_t x = (static_cast<uint64_t>(hi) << 32) | lo;
         return DMUL(DADD(static_cast<double>(x >> 12), 0.5), 0x1p-52);
