@@ -84,6 +84,20 @@ struct Stream {
     __device__ __forceinline__ double next_normal() { return qrmc_normal_quantile(next_uniform()); }
 };
 
+// qrmc_normal_quantile with PPND16's two branches evaluated side by side and selected
+// (the same operations on every value, so the same double): for a warp that holds both
+// central and tail lanes -- nearly every warp -- the divergent form runs the branches one
+// after the other, this form issues the two dependent chains interleaved, which shortens
+// a latency-bound producer's critical path.
+__device__ __forceinline__ double normal_quantile_ilp(double p) {
+    const double pp = QRMC_MUL(0.5, QRMC_MUL(2.0, p));  // erfc_inv(2p)'s argument to PPND16
+    const double q = QRMC_SUB(pp, 0.5);
+    const double c = qrmc_ppnd16_central(q);
+    const double t = qrmc_ppnd16_tail(q < 0 ? pp : QRMC_SUB(1.0, pp));
+    const double v = (q < 0 ? -q : q) <= 0.425 ? c : (q < 0 ? -t : t);
+    return QRMC_MUL(-QRMC_ROOT_TWO, QRMC_DIV(-v, QRMC_ROOT_TWO));
+}
+
 __device__ __forceinline__ uint64_t sid_training(int step, uint64_t path) {
     return (static_cast<uint64_t>(step) << kStepShift) | path;
 }

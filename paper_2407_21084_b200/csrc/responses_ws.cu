@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
 #endif
         for (int l = pw; l < D; l += kWsProducers) {
 #ifndef QRMC_WS_EXP_NOEULER
-            const double nrm = qrmc_normal_quantile(
+            const double nrm = normal_quantile_ilp(
                 u64_to_uniform(stream_u64_at(a.seed, sid, static_cast<uint64_t>(D) * (j - i0 + 1) + l)));
 #else
             const double nrm = 0.001 * (j + l);
