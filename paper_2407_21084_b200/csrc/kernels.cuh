@@ -96,9 +96,12 @@ constexpr int kWsConsumers = 16;
 constexpr int kWsProducers = 4;
 constexpr int kWsPaths = 32;    // paths per CTA (4 row blocks of 8)
 #ifndef QRMC_WS_PREFETCH
-#define QRMC_WS_PREFETCH 4
+#define QRMC_WS_PREFETCH 1
 #endif
-constexpr int kWsPrefetch = QRMC_WS_PREFETCH;  // fragments the L1 prefetch runs ahead
+// fragments the L1 prefetch runs ahead (M = 2e6: 0 / 1 / 2 / 4 ahead = 0.727 / 0.708 /
+// 0.711 / 0.712 s K1; with ~2 KB of L1 beside the tables, lines fetched further ahead are
+// evicted before use)
+constexpr int kWsPrefetch = QRMC_WS_PREFETCH;
 
 struct WsArgs {
     const double* alpha;      // fragment streams, warp-major: warp w's series 0..N-1 back to back
