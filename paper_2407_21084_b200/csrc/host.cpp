@@ -1056,6 +1056,8 @@ struct qrmc_gpu_plan {
     ProjMmaArgs pmma{};
     DevBuf<int4> d_pm_rects;
     DevBuf<int32_t> d_pm_out;
+    DevBuf<double> d_pm_scratch;  // K2 split halves (ProjMmaArgs::split)
+    DevBuf<int> d_pm_counters;
     DevBuf<double> d_alpha_mma;
     DevBuf<int4> d_mma_units, d_mma_warps;
     DevBuf<uint32_t> d_mma_terms;
@@ -1442,6 +1444,29 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                     }
                     pm.basis_size = P->K;
                     pm.batch = pbatch;
+                    // split each lane's chunks over two CTAs when that fills the last wave of
+                    // CTAs (one CTA per SM) noticeably better: Gamma_H(4,100) on 148 SMs runs
+                    // 2 x 256 CTAs = 3.46 waves (87% of 4 busy), split 6.92 waves (99% of 7)
+                    {
+                        int sms = 0;
+                        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device), "attr");
+                        const char* ks = std::getenv("QRMC_K2_SPLIT");
+                        // decided on the single-GPU grid (all 256 lanes) whatever the world size:
+                        // the split changes the rounding of the lane sums, and alpha must be
+                        // bitwise independent of the GPU count
+                        const double w1 = static_cast<double>(L.proj_parts) * kLanes / std::max(sms, 1);
+                        const double e1 = w1 / std::ceil(w1), e2 = 2 * w1 / std::ceil(2 * w1);
+                        pm.split = ks ? (std::atoi(ks) == 2 ? 2 : 1) : (e2 > e1 + 0.02 ? 2 : 1);
+                        if (pm.split == 2) {
+                            P->d_pm_scratch.alloc(static_cast<size_t>(2) * kLanes * L.proj_parts * kProjWarps *
+                                                  kProjTiles * 64);
+                            P->d_pm_counters.alloc(static_cast<size_t>(kLanes) * L.proj_parts);
+                            cuda_check(cudaMemsetAsync(P->d_pm_counters.p, 0, P->d_pm_counters.n * sizeof(int), st),
+                                       "memset");
+                            pm.scratch = P->d_pm_scratch.p;
+                            pm.counters = P->d_pm_counters.p;
+                        }
+                    }
                     cuda_check(configure_project_mma(d, pbatch, psmem), "k_project_mma attributes");
                     P->base.cloud_cos = 1;  // K1 stores cos(pi F(x)) for this K2
                     P->h2d_bytes += L.proj_rects.size() * sizeof(int4) + L.proj_out.size() * sizeof(int32_t);

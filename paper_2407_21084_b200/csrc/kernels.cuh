@@ -144,6 +144,11 @@ struct ProjMmaArgs {
     int kmax[kMaxDim];
     int64_t basis_size;
     int batch;                // kProjBatchWide or kProjBatchNarrow (project_mma_batch)
+    // split = 2: each lane's chunks in two halves on two CTAs (grid z), combined as
+    // half 0 + half 1 by the CTA that finishes second (fills the last wave of CTAs)
+    int split;
+    double* scratch;          // [2][owned_lanes][parts][kProjWarps][kProjTiles][64] (split = 2)
+    int* counters;            // [owned_lanes][parts], zero between launches (split = 2)
     double* partials;         // [owned_lanes][K]
 };
 

@@ -59,6 +59,7 @@ struct BatchGeom {
 template <int B>
 struct ProjSmem {
     double s[2][B];  // S_m of the batch (0 past the chunk's end)
+    int second;      // split = 2: this CTA finished its lane's second half
     // followed by two cosine-table buffers [table_len][B + 4]
 };
 
@@ -122,11 +123,17 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
     const int64_t chunks_total = (a.paths + kChunk - 1) / kChunk;
     const int64_t my_chunks = (chunks_total - (a.lane_lo + lane_rel) + kLanes - 1) / kLanes;
     const int n_batches = static_cast<int>(my_chunks) * BatchGeom<B>::kPerChunk;
+    // split = 2: half z takes chunks [0, ceil(c/2)) or the rest (a chunk boundary, so the
+    // halves -- and the bits -- do not depend on the batch width B)
+    const int half = blockIdx.z;
+    const int hb = static_cast<int>((my_chunks + 1) / 2) * BatchGeom<B>::kPerChunk;
+    const int b_lo = p.split == 2 && half == 1 ? hb : 0;
+    const int b_hi = p.split == 2 && half == 0 ? hb : n_batches;
     // cos theta_l (and S) of this thread's task in batch b, fetched a batch ahead
     auto fetch = [&](int b, double& c1, double& sv) {
         c1 = 1.0;
         sv = 0.0;
-        if (b >= n_batches || tid >= kTasks) return;
+        if (b >= b_hi || tid >= kTasks) return;
         {
             const Batch bt = lane_batch<B>(a, lane_rel, b);
             if (pt >= bt.n) return;
@@ -155,14 +162,14 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
     };
 
     double cn, sn;
-    fetch(0, cn, sn);
+    fetch(b_lo, cn, sn);
     build(0, cn, sn);
-    fetch(1, cn, sn);
+    fetch(b_lo + 1, cn, sn);
     batch_barrier();
-    for (int b = 0; b < n_batches; ++b) {
-        const int buf = b & 1;
+    for (int b = b_lo; b < b_hi; ++b) {
+        const int buf = (b - b_lo) & 1;
         // tables of batch b+1 (other buffer) while the tensor cores take batch b
-        if (b + 1 < n_batches) {
+        if (b + 1 < b_hi) {
             build(buf ^ 1, cn, sn);
             fetch(b + 2, cn, sn);
         }
@@ -207,6 +214,48 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
     // partial[lane][k] = sqrt2^{nnz(k)} G[u][t]
     double* out = p.partials + static_cast<int64_t>(lane_rel) * p.basis_size;
     const int32_t* om = p.out + static_cast<int64_t>(slot) * kProjTiles * 64;
+    if (p.split == 2) {
+        // both halves park their tiles; the CTA that arrives second writes half 0 + half 1
+        const size_t cta_vals = static_cast<size_t>(kProjWarps) * kProjTiles * 64;
+        const size_t at = (static_cast<size_t>(lane_rel) * gridDim.x + blockIdx.x) * cta_vals +
+                          static_cast<size_t>(threadIdx.x >> 5) * kProjTiles * 64;
+        const size_t half_vals = static_cast<size_t>(gridDim.y) * gridDim.x * cta_vals;
+        double* mine = p.scratch + half * half_vals + at;
+#pragma unroll
+        for (int ig = 0; ig < NG; ++ig)
+#pragma unroll
+            for (int it = 0; it < NT; ++it)
+                if (it < nt) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) mine[(ig * nt + it) * 64 + lane * 2 + h] = acc[ig][it][h];
+                }
+        __threadfence();
+        batch_barrier();
+        if (threadIdx.x == 0) {
+            int* ctr = p.counters + static_cast<size_t>(lane_rel) * gridDim.x + blockIdx.x;
+            const int old = atomicAdd(ctr, 1);
+            sm.second = old == 1;
+            if (old == 1) *ctr = 0;  // both halves are in: ready for the next launch
+        }
+        batch_barrier();
+        if (!sm.second) return;
+        __threadfence();
+        const double* h0 = p.scratch + at;
+        const double* h1 = p.scratch + half_vals + at;
+#pragma unroll
+        for (int ig = 0; ig < NG; ++ig)
+#pragma unroll
+            for (int it = 0; it < NT; ++it)
+                if (it < nt) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int k = __ldg(&om[(ig * nt + it) * 64 + lane * 2 + h]);
+                        const int e = (ig * nt + it) * 64 + lane * 2 + h;
+                        if (k >= 0) out[k] = DMUL(DADD(__ldcg(h0 + e), __ldcg(h1 + e)), __ldg(&p.scale[k]));
+                    }
+                }
+        return;
+    }
 #pragma unroll
     for (int ig = 0; ig < NG; ++ig)
 #pragma unroll
@@ -300,7 +349,8 @@ cudaError_t configure_project_mma(int dim, int batch, size_t smem) {
 
 cudaError_t launch_project_mma(const StepArgs& a, const ProjMmaArgs& p, cudaStream_t st) {
     if (a.owned_lanes == 0 || p.parts == 0) return cudaSuccess;
-    const dim3 grid(static_cast<unsigned>(p.parts), static_cast<unsigned>(a.owned_lanes));
+    const dim3 grid(static_cast<unsigned>(p.parts), static_cast<unsigned>(a.owned_lanes),
+                    static_cast<unsigned>(p.split == 2 ? 2 : 1));
     return with_project_kernel(a.prob.dim, p.batch, a.meas.form == 3, [&](auto kern) {
         kern<<<grid, kThreads, project_mma_smem_bytes(p.table_len, p.batch), st>>>(a, p);
         return cudaGetLastError();

@@ -292,6 +292,19 @@ def test_ring_tensor_core_k1_matches_reference(L, entry, monkeypatch):
     assert (stats.applications, stats.clipped) == (entry["applications"], entry["clipped"])
 
 
+@pytest.mark.parametrize("split", ["1", "2"])
+def test_k2_lane_split_matches_port(L, port, monkeypatch, split):
+    # K2's two-CTA lane split (half 0 + half 1, combined by the later CTA) and the single
+    # CTA per lane both reproduce the restatement; M gives lanes of 1 and 2 chunks
+    monkeypatch.setenv("QRMC_K2_SPLIT", split)
+    prob = _abi.sin_bench_problem(4)
+    cfg = _abi.ConfigHolder(steps=3, paths=300_000, damping=5.1, seed=19, gamma_kind=2, degrees=[20])
+    coeffs, stats, _ = api.backward_solve(prob, cfg)
+    ref, rs = port.backward_solve(prob, cfg, coeffs.shape[1])
+    assert float(np.abs(coeffs - ref).max()) / max(1.0, float(np.abs(ref).max())) <= ALPHA_TOL
+    assert (stats.applications, stats.clipped) == (rs.applications, rs.clipped)
+
+
 @pytest.mark.parametrize("dim,deg,paths", [(3, 8, 5000), (4, 100, 3000), (6, 16, 2051)])
 def test_k2_batch_width_does_not_change_bits(L, monkeypatch, dim, deg, paths):
     # K2 stages 24 paths per shared-memory batch (16 when those tables do not fit);

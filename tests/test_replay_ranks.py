@@ -67,6 +67,22 @@ def test_every_world_is_bitwise_equal_to_the_single_rank_solve(c, world):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("split", ["1", "2"])
+@pytest.mark.parametrize("world", [2, 8])
+def test_k2_lane_split_keeps_worlds_bitwise_equal(monkeypatch, split, world):
+    # K2 may split each lane's chunks over two CTAs (QRMC_K2_SPLIT; host.cpp decides on the
+    # 256-lane grid whatever the world size), so both settings must stay G-independent
+    monkeypatch.setenv("QRMC_K2_SPLIT", split)
+    prob = _abi.sin_bench_problem(4)
+    cfg = _abi.ConfigHolder(steps=4, paths=400_003, damping=5.1, seed=77, gamma_kind=2, degrees=[40])
+    ref, rs, _ = api.backward_solve(prob, cfg)
+    st, got, gs, msg = replay(prob, cfg, world)
+    assert st == _abi.OK, msg
+    np.testing.assert_array_equal(got, ref)
+    assert (gs.applications, gs.clipped) == (rs.applications, rs.clipped)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("world", [1, 3])
 def test_errors_are_global_across_ranks(world):
     """A SimulationError on any path fails the whole solve with the smallest step,
