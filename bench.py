@@ -303,10 +303,16 @@ def run_srmc(args, world: int, rank: int, local: int, dist) -> dict:
                               "note": "per GPU; path generation (Philox, AS241 quantiles) dominates; HBM traffic "
                                       "per path-step is ~2P*8/M bytes (table read + write), far below the ridge"}}
         if world == 1:
-            # e2e: the public one-shot call with host tables (allocation, solve, D2H of every step's table)
-            t0 = time.perf_counter()
-            tab = srmc.solve(p, c)
-            e2e = time.perf_counter() - t0
+            # e2e: the public one-shot call with host tables (allocation, solve, D2H of every
+            # step's table), one untimed call first (first-touch of the host pages), then the
+            # median of 2
+            del srmc.solve(p, c).y
+            e2es = []
+            for _ in range(2):
+                t0 = time.perf_counter()
+                tab = srmc.solve(p, c)
+                e2es.append(time.perf_counter() - t0)
+            e2e = statistics.median(e2es)
             entry["e2e"] = {"value": ps / e2e, "unit": "path-steps/s", "h2d_bytes_per_step": 0,
                             "d2h_bytes_per_step": int(tab.y.nbytes)}
             del tab
