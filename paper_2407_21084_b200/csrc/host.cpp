@@ -730,8 +730,10 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
         const char* e = std::getenv(n);
         return e ? std::atof(e) : v;
     };
-    const double cost_step = env_or("QRMC_COST_STEP", 16.0), cost_nb = env_or("QRMC_COST_NB", 10.0),
-                 cost_epi = env_or("QRMC_COST_EPI", 48.0);
+    // (warp-specialised layout: (12, 10, 64) measured 0.705 s vs 0.708-0.710 for (16, 10, 48)
+    // at the bench shape, M = 2e6; the ring kernel keeps (16, 10, 48))
+    const double cost_step = env_or("QRMC_COST_STEP", opt.ring ? 16.0 : 12.0), cost_nb = env_or("QRMC_COST_NB", 10.0),
+                 cost_epi = env_or("QRMC_COST_EPI", opt.ring ? 48.0 : 64.0);
     auto add_units = [&](int cb, int nb, int lo, int hi) {  // chunk range [lo, hi) of cbs cb..cb+nb-1
         if (hi <= lo) return;
         const int np = (hi - lo + kMmaKSplit - 1) / kMmaKSplit;
