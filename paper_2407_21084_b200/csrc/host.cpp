@@ -527,6 +527,7 @@ struct MmaLayoutOpts {
     // over the groups (units with nb = 8 + tail_terms / 8, responses_ws.cu ws_unit_t): no
     // per-unit epilogue for the hyperbolic tail's many small groups
     int tail_terms = 0;
+    int bundle = kMmaBundle;    // max column blocks per unit
 };
 
 struct MmaLayout {
@@ -762,14 +763,14 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
         if (QRMC_MMA_STAIR) {
             // staircase bundles: kMmaBundle consecutive column blocks share the chunks
             // all of them have; each block's remainder runs in narrower units
-            e = std::min(tail_cb, cb + kMmaBundle);
+            e = std::min(tail_cb, cb + opt.bundle);
             int lo = 0;
             for (int k = e; k > cb; --k) {  // blocks cb..k-1 share [lo, E_{k-1})
                 add_units(cb, k - cb, lo, cb_chunks[k - 1]);
                 lo = std::max(lo, cb_chunks[k - 1]);
             }
         } else {
-            while (e < tail_cb && e - cb < kMmaBundle && cb_chunks[e] == cb_chunks[cb]) ++e;
+            while (e < tail_cb && e - cb < opt.bundle && cb_chunks[e] == cb_chunks[cb]) ++e;
             add_units(cb, e - cb, 0, cb_chunks[cb]);
         }
         cb = e;
@@ -1367,6 +1368,7 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                     o.ring = false;
                     o.bank_order = 1;
                     o.tail_terms = ws_tail_terms();
+                    o.bundle = QRMC_WS_BUNDLE;
                     MmaLayout W = build_mma_layout(P->gamma, pa.offset, o);
                     if (W.ok) {
                         P->use_ws = true;
@@ -1744,6 +1746,7 @@ qrmc_status qrmc_gpu_mma_layout_check(int32_t kind, int32_t dim, const int32_t* 
             o.ring = false;
             o.bank_order = 1;
             o.tail_terms = tail;
+            o.bundle = QRMC_WS_BUNDLE;
             const MmaLayout W = build_mma_layout(g, offset, o);
             if (!W.ok) fail(QRMC_ELOGIC, "ws layout: not a chain although the mma layout is");
             std::vector<double> wtab(static_cast<size_t>(off) * 32, 0.0);

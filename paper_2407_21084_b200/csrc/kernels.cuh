@@ -92,6 +92,9 @@ struct MmaArgs {
 // warps run the Euler steps, the x-only parts, the truncation/driver of
 // evaluation j-2 and the tables of evaluation j+1 into the other buffer; the
 // hand-off uses named barriers. B fragments stream from L2 (prefetched to L1).
+#ifndef QRMC_WS_BUNDLE
+#define QRMC_WS_BUNDLE 2  // column blocks per warp-specialised unit (ws_unit<D, NB>, NB <= 3)
+#endif
 constexpr int kWsConsumers = 16;
 constexpr int kWsProducers = 4;
 constexpr int kWsPaths = 32;    // paths per CTA (4 row blocks of 8)

@@ -405,6 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
                     ws_unit<D, 1>(m, un.x, un.z, un.w, bsrc, trow, half, col, y);
                 else if (un.y == 2)
                     ws_unit<D, 2>(m, un.x, un.z, un.w, bsrc, trow, half, col, y);
+#if QRMC_WS_BUNDLE >= 3
+                else if (un.y == 3)
+                    ws_unit<D, 3>(m, un.x, un.z, un.w, bsrc, trow, half, col, y);
+#endif
                 else if (un.y == 9)
                     ws_unit_t<D, 1>(m, un.z, un.w, bsrc, trow, half, col, y);
                 else
