@@ -22,6 +22,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -239,13 +240,19 @@ def run_reference_arm(args) -> int:
 
 # ------------------------------------------------------------------ SRMC (row f3)
 # The north_star's stratified regression Monte Carlo solver at the literal BASELINE.json
-# configs 2 and 4 (include/qrmc_srmc.h; no reference arm: the reference has no SRMC).
+# configs 2 and 4, and config 3 (Bergman) at tools/srmc_bench.py's shape
+# (include/qrmc_srmc.h; no reference arm: the reference has no SRMC).
 # Hypercubes are partitioned over the ranks and every step's table is all-gathered
 # (strong scaling: the cell count is the config's, whatever N).
 SRMC_WORKLOADS = {
     "config2": ("sin-d4-lp1-40^4-N20-M1000", 4, dict(steps=20, cells_per_dim=40, paths_per_cell=1000, basis=1)),
     "config4": ("sin-d6-lp0-16^6-N10-M100", 6, dict(steps=10, cells_per_dim=16, paths_per_cell=100, basis=0)),
 }
+# BASELINE config 3 (Bergman borrowing/lending, d=4, LP1, N=20; the hypercubes and paths
+# are this repo's choice, tools/srmc_bench.py): a z-dependent driver, so two passes per step
+SRMC_BERGMAN = ("bergman-d4-lp1-24^4-N20-M500", 4,
+                dict(steps=20, cells_per_dim=24, paths_per_cell=500, basis=1, lo=math.log(100) - 0.6,
+                     hi=math.log(100) + 0.6))
 DFMA_PEAK_TFLOPS = 34.2  # builder-measured scalar DFMA peak (profiles/r01_fp64_peak.txt); SRMC runs no tensor op
 
 
@@ -260,12 +267,28 @@ def srmc_flops_per_path_step(d: int, P: int) -> int:
     return 5 * d + 35 * d + 4 * d + 7 * d + 2 * P + (d + 7) + P * (P + 1) + 2 + 2 * P
 
 
+def srmc_bergman_flops_per_path_step(d: int, P: int) -> int:
+    """The Bergman scheme per path-step, counted the same way: two passes over the same
+    draws (include/qrmc_srmc.h). Pass 1: path (start 5d, quantiles 35d, Euler 4d, cell 7d),
+    next-step polynomial 2P, Gram P(P+1), Z right-hand side d (2 + 2P). Pass 2: the path
+    again (51d + 2P), Z_hat at the start d * 2P, driver 3d + 12 (sum of z, borrow/lend
+    rates), Y right-hand side 2 + 2P."""
+    path = 5 * d + 35 * d + 4 * d + 7 * d + 2 * P
+    return (path + P * (P + 1) + d * (2 + 2 * P)) + (path + d * 2 * P + 3 * d + 12 + 2 + 2 * P)
+
+
 def run_srmc(args, world: int, rank: int, local: int, dist) -> dict:
     import torch
     from paper_2407_21084_b200 import srmc
     out = {}
-    for key, (name, d, kw) in SRMC_WORKLOADS.items():
-        p, c = srmc.sin_bench_problem(d), srmc.config(**kw)
+    todo = {k: (name, d, kw, srmc.sin_bench_problem(d), srmc_flops_per_path_step)
+            for k, (name, d, kw) in SRMC_WORKLOADS.items()}
+    bname, bd, bkw = SRMC_BERGMAN
+    todo["config3"] = (bname, bd, bkw, srmc.bergman_problem(bd, 0.05, 0.2, 0.01, 0.06, 100.0, 0.5),
+                       srmc_bergman_flops_per_path_step)
+    for key in ("config2", "config3", "config4"):
+        name, d, kw, p, flops_fn = todo[key]
+        c = srmc.config(**kw)
         nid = None
         if world > 1:
             obj = [srmc.nccl_unique_id() if rank == 0 else None]
@@ -290,9 +313,10 @@ def run_srmc(args, world: int, rank: int, local: int, dist) -> dict:
         cells = kw["cells_per_dim"] ** d
         ps = cells * kw["paths_per_cell"] * kw["steps"]  # whole job (all ranks)
         P = d + 1 if kw["basis"] == 1 else 1
-        fl = srmc_flops_per_path_step(d, P)
+        fl = flops_fn(d, P)
         entry = {"workload": name, "value": ps / t, "unit": "path-steps/s", "seconds_per_solve": t,
                  "cells": cells, "paths_per_cell": kw["paths_per_cell"], "N": kw["steps"], "basis": f"LP{kw['basis']}",
+                 "path_passes": 2 if key == "config3" else 1,  # a path-step counts once either way
                  "n_gpus": world, "scaling": "strong (fixed hypercubes, partitioned over the ranks)",
                  "exchange": "ncclAllGather of every step's y table" if world > 1 else "none (1 rank)",
                  "clocks": clocks.summary(),
