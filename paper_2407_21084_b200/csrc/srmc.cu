@@ -299,9 +299,13 @@ __device__ __forceinline__ void acc_gram(double* A, const double* phi) {
 // WANTZ: fit Z alongside Y in a single pass (driver without z).
 // G lanes per hypercube: 32 (one warp) normally, 8 when M is small so the per-cell
 // butterfly + Cholesky is amortised over more path iterations per lane.
-template <int D, int P, bool ZPASS, bool WANTZ, int G>
+// CACHE (ZPASS with the Bergman driver, which reads y and Z_hat but not x): pass 1 parks
+// each path's (Y1, local coordinates) in dynamic shared memory and pass 2 reads them back
+// instead of regenerating the path (the same doubles, so the same tables).
+template <int D, int P, bool ZPASS, bool WANTZ, int G, bool CACHE = false>
 __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P >= 20 ? 1 : 2))) k_srmc_step(SrmcDev s, const double* __restrict__ next,
                                                    double* __restrict__ ytab, double* __restrict__ ztab) {
+    static_assert(!CACHE || ZPASS, "the path cache serves the second pass");
     constexpr int NA = P * (P + 1) / 2;
     constexpr bool ANYZ = ZPASS || WANTZ;
     const int lane = threadIdx.x & 31;
@@ -345,9 +349,17 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
     const int64_t iters = (s.M + G - 1) / G;
     double x0[D], sl[D], dw[D], x1[D], phi[P], y1;
     const double zero_z[D] = {};
+    extern __shared__ double path_cache[];  // CACHE: [warp][it][1 + D][32 lanes]
+    double* pc = path_cache + static_cast<size_t>(threadIdx.x >> 5) * iters * (1 + D) * 32 + lane;
     for (int64_t it = 0; it < iters; ++it) {
         const int64_t m = sub + it * G;
         srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1, scratch);
+        if constexpr (CACHE) {
+            double* e = pc + it * (1 + D) * 32;
+            e[0] = y1;
+#pragma unroll
+            for (int l = 0; l < D; ++l) e[(1 + l) * 32] = sl[l];
+        }
         if (m >= mend) continue;
         phi_of<D, P>(sl, phi);
         acc_gram<D, P>(A, phi);
@@ -373,8 +385,16 @@ __global__ void __launch_bounds__(256, (P == 1 ? 3 : ((ZPASS || WANTZ) && D * P 
     if constexpr (ZPASS) {
         for (int64_t it = 0; it < iters; ++it) {
             const int64_t m = sub + it * G;
-            srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1, scratch);
-            if (m >= mend) continue;
+            if constexpr (CACHE) {
+                if (m >= mend) continue;
+                const double* e = pc + it * (1 + D) * 32;
+                y1 = e[0];
+#pragma unroll
+                for (int l = 0; l < D; ++l) sl[l] = e[(1 + l) * 32];
+            } else {
+                srmc_path<D, P>(s, next, cc, k, m, x0, sl, dw, x1, y1, scratch);
+                if (m >= mend) continue;
+            }
             phi_of<D, P>(sl, phi);
             double zi[D];
 #pragma unroll
@@ -488,6 +508,8 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
     return s;
 }
 
+constexpr size_t kSrmcCacheBytes = 192 * 1024;  // + 8 warps' tail scratch stays under 227 KB
+
 template <int D, int P>
 void launch_step_t(const SrmcDev& s, const double* next, double* y, double* z, bool zpass, bool wantz, cudaStream_t st) {
     const int warps = 8;
@@ -512,6 +534,14 @@ void launch_step_t(const SrmcDev& s, const double* next, double* y, double* z, b
     }
     const unsigned grid = static_cast<unsigned>((cells + warps - 1) / warps);
     if (grid == 0) return;
+    // the Bergman second pass from a shared-memory path cache when it fits (M <= ~640 at d=4)
+    const size_t cache = static_cast<size_t>(warps) * ((s.M + 31) / 32) * (1 + D) * 32 * sizeof(double);
+    if (zpass && s.kind == QRMC_SRMC_BERGMAN && cache <= kSrmcCacheBytes &&
+        cudaFuncSetAttribute(k_srmc_step<D, P, true, false, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSrmcCacheBytes)) == cudaSuccess) {
+        k_srmc_step<D, P, true, false, 32, true><<<grid, warps * 32, cache, st>>>(s, next, y, z);
+        return;
+    }
     if (zpass)
         k_srmc_step<D, P, true, false, 32><<<grid, warps * 32, 0, st>>>(s, next, y, z);
     else if (wantz)
