@@ -95,7 +95,10 @@ struct MmaArgs {
 #ifndef QRMC_WS_BUNDLE
 #define QRMC_WS_BUNDLE 2  // column blocks per warp-specialised unit (ws_unit<D, NB>, NB <= 3)
 #endif
-constexpr int kWsConsumers = 16;
+#ifndef QRMC_WS_CONSUMERS
+#define QRMC_WS_CONSUMERS 16
+#endif
+constexpr int kWsConsumers = QRMC_WS_CONSUMERS;  // a power of two (the finish's pairwise sum)
 constexpr int kWsProducers = 4;
 constexpr int kWsPaths = 32;    // paths per CTA (4 row blocks of 8)
 #ifndef QRMC_WS_PREFETCH
