@@ -21,6 +21,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -480,6 +481,10 @@ SrmcDev make_dev(const qrmc_srmc_problem_t* p, const qrmc_srmc_config_t* c) {
     s.k0 = 0;
     s.k1 = s.cells;
     s.seed = c->seed;
+    {
+        const char* e = std::getenv("QRMC_SRMC_PATH_CACHE");
+        s.path_cache = !(e && e[0] == '0');
+    }
     for (int r = 0; r < 10; ++r) {  // Philox4x32-10 key schedule (rng.cpp:9-40)
         s.rk[2 * r] = static_cast<uint32_t>(c->seed) + static_cast<uint32_t>(r) * 0x9E3779B9u;
         s.rk[2 * r + 1] = static_cast<uint32_t>(c->seed >> 32) + static_cast<uint32_t>(r) * 0xBB67AE85u;
@@ -536,7 +541,7 @@ void launch_step_t(const SrmcDev& s, const double* next, double* y, double* z, b
     if (grid == 0) return;
     // the Bergman second pass from a shared-memory path cache when it fits (M <= ~640 at d=4)
     const size_t cache = static_cast<size_t>(warps) * ((s.M + 31) / 32) * (1 + D) * 32 * sizeof(double);
-    if (zpass && s.kind == QRMC_SRMC_BERGMAN && cache <= kSrmcCacheBytes &&
+    if (zpass && s.kind == QRMC_SRMC_BERGMAN && s.path_cache && cache <= kSrmcCacheBytes &&
         cudaFuncSetAttribute(k_srmc_step<D, P, true, false, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kSrmcCacheBytes)) == cudaSuccess) {
         k_srmc_step<D, P, true, false, 32, true><<<grid, warps * 32, cache, st>>>(s, next, y, z);

@@ -26,6 +26,7 @@ struct SrmcDev {
     // interleaves their bits, coordinate d-1 lowest, so a 6-D neighbourhood sits in a few
     // nearby rows of the table and the concurrently processed cells' gathers stay in L2.
     // Cells are visited in row order; draws stay keyed by the lexicographic cell index.
+    int path_cache;   // Bergman second pass from the shared-memory path cache (QRMC_SRMC_PATH_CACHE=0: off)
     int morton, mbits;
     uint32_t mmul, mmask;  // spread(c) = (c * mmul) & mmask puts bit b of c at b*D (exact: mbits <= D-1)
 };

@@ -294,3 +294,18 @@ def test_ppnd16_split_branches_equal_the_whole():
     whole, split = np.zeros_like(u), np.zeros_like(u)
     f(u.ctypes.data_as(dp), u.size, whole.ctypes.data_as(dp), split.ctypes.data_as(dp))
     np.testing.assert_array_equal(whole, split)
+
+
+@pytest.mark.gpu
+def test_gpu_bergman_path_cache_gives_the_same_tables(monkeypatch):
+    """The Bergman second pass reads each path's (Y1, local coordinates) from a shared-memory
+    cache written by the first pass (srmc.cu, M small enough); regenerating the path instead
+    (QRMC_SRMC_PATH_CACHE=0) must give the same bits."""
+    p = _bergman(4, 0.01, 0.06)
+    lo, hi = _box()
+    c = srmc.config(steps=3, cells_per_dim=6, paths_per_cell=300, basis=srmc.LP1, lo=lo, hi=hi, seed=5)
+    a = srmc.solve(p, c, with_z=True)
+    monkeypatch.setenv("QRMC_SRMC_PATH_CACHE", "0")
+    b = srmc.solve(p, c, with_z=True)
+    np.testing.assert_array_equal(a.y, b.y)
+    np.testing.assert_array_equal(a.z, b.z)
