@@ -38,6 +38,9 @@ import numpy as np  # noqa: E402
 
 WORKLOAD = dict(name="sinbench-d4-hyperbolic100-q5.1-N20", dim=4, kappa=0.6, lam=0.0, horizon=1.0,
                 gamma_kind="hyperbolic", degrees=(100,), damping=5.1, steps=20, mu=2.0, seed=42)
+# BASELINE config 4 restated for GQRMDP: d=6, Gamma_H(6,64) (K=76,433), N=10,
+# M = 2e7 per GPU -- a second line in the JSON (`gqrmdp_config4`), one timed solve
+WORKLOAD_C4 = dict(WORKLOAD, name="sinbench-d6-hyperbolic64-q5.1-N10", dim=6, degrees=(64,), steps=10)
 DEFAULT_PATHS_PER_GPU = 20_000_000
 CPU_SAMPLE_PATHS = 16_384  # 16 lanes of 1024 paths: saturates 16 host cores (parallel.hpp:21-22)
 METRIC = "simulated paths x time-steps per second per full backward solve"
@@ -130,9 +133,9 @@ def flops_alg(k: int, m: int, n: int) -> float:
     return float(k) * m * n * (n + 1)
 
 
-def make_problem_config(paths: int):
+def make_problem_config(paths: int, w: dict | None = None):
     from paper_2407_21084_b200 import _abi
-    w = WORKLOAD
+    w = w or WORKLOAD
     prob = _abi.sin_bench_problem(w["dim"], w["kappa"], w["lam"], w["horizon"])
     cfg = _abi.ConfigHolder(steps=w["steps"], paths=paths, damping=w["damping"], seed=w["seed"],
                             gamma_kind=_abi.GAMMA_KINDS[w["gamma_kind"]], degrees=w["degrees"], mu=w["mu"])
@@ -344,6 +347,52 @@ def run_srmc(args, world: int, rank: int, local: int, dist) -> dict:
     return out
 
 
+def run_gqrmdp_config4(args, L, session, world: int, dist) -> dict:
+    """BASELINE config 4 restated for GQRMDP on the same session: one warm-up and one timed
+    solve (device time, max over ranks), per-kernel seconds and the dominant kernel's FP64
+    fraction (the same algorithmic count as the headline: 2 K FLOPs per evaluation)."""
+    import torch
+    from paper_2407_21084_b200 import api
+    err = C.create_string_buffer(1024)
+    m = args.paths
+    n = WORKLOAD_C4["steps"]
+    prob, cfg = make_problem_config(m * world, WORKLOAD_C4)
+    plan = C.c_void_p()
+    api.raise_for(L.qrmc_gpu_plan_create(session, C.byref(prob), cfg.ref(), C.byref(plan), err, 1024),
+                  err.value.decode())
+    stats = _abi_stats()
+    try:
+        times, ks = [], (C.c_double * 3)()
+        for _ in range(2):  # warm-up, timed
+            if dist is not None:
+                dist.barrier()
+            api.raise_for(L.qrmc_gpu_plan_run(plan, C.byref(stats), err, 1024), err.value.decode(), stats.error_step)
+            times.append(stats.device_seconds)
+        t = times[-1]
+        L.qrmc_gpu_plan_kernel_seconds(plan, ks, None, err, 1024)
+        if dist is not None:
+            tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        K = int(L.qrmc_gpu_plan_basis_size(plan))
+        names = [L.qrmc_gpu_plan_kernel_name(plan, w).decode() for w in range(3)]
+    finally:
+        L.qrmc_gpu_plan_destroy(plan)
+    k1 = 2.0 * K * m * n * (n - 1) / 2.0 / ks[0] / 1e12
+    return {"workload": WORKLOAD_C4["name"], "value": path_steps(m * world, n) / t, "unit": UNIT,
+            "seconds_per_solve": t, "basis_size": K, "N": n, "paths_per_gpu": m, "n_gpus": world,
+            "kernel_seconds_per_solve": dict(zip(names, ks[:])),
+            "roofline": {"kernel": names[0], "bound": "fp64", "achieved": k1, "peak": peaks()["fp64_tflops"],
+                         "unit": "TFLOP/s", "frac": k1 / peaks()["fp64_tflops"],
+                         "peak_source": "of builder-measured 37.1 TF/s FP64 (profiles/r01_fp64_peak.txt)"},
+            "timing": "one solve after one warm-up (device time, CUDA events)"}
+
+
+def _abi_stats():
+    from paper_2407_21084_b200 import _abi
+    return _abi.Stats()
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args) -> int:
     from paper_2407_21084_b200 import _abi, api
@@ -445,6 +494,7 @@ def run_ours(args) -> int:
     names = [L.qrmc_gpu_plan_kernel_name(plan, w).decode() for w in range(3)]
     L.qrmc_gpu_plan_destroy(plan)
 
+    c4_line = None if args.no_config4 else run_gqrmdp_config4(args, L, session, world, dist)
     srmc_line = None if args.no_srmc else run_srmc(args, world, rank, local, dist)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -481,6 +531,8 @@ def run_ours(args) -> int:
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if c4_line is not None:
+            line["gqrmdp_config4"] = c4_line
         if srmc_line is not None:
             line["srmc"] = srmc_line
         print(json.dumps(line), flush=True)
@@ -500,6 +552,7 @@ def main() -> int:
     ap.add_argument("--cpu-paths", type=int, default=CPU_SAMPLE_PATHS)
     ap.add_argument("--cpu-repeats", type=int, default=3)
     ap.add_argument("--no-srmc", action="store_true", help="skip the SRMC (row f3) section")
+    ap.add_argument("--no-config4", action="store_true", help="skip the GQRMDP config-4 restatement")
     ap.add_argument("--srmc-steps", type=int, default=3)
     ap.add_argument("--srmc-warmup", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=1)
