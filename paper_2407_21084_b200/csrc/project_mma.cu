@@ -157,7 +157,9 @@ __device__ __forceinline__ void project_rect(const StepArgs& a, const ProjMmaArg
     };
     auto build = [&](int buf, double c1, double sv) {
         if (tid >= kTasks) return;
+#ifndef QRMC_PROJ_EXP_NOTAB  // timing experiments only (wrong results)
         cos_table_piece_c(c1, p.kmax[tl], tq, TS, tabs0 + buf * tab_elems + p.offset[tl] * kStride + pt, kStride);
+#endif
         if (tq == 0 && tl == 0) sm.s[buf][pt] = sv;
     };
 
