@@ -619,18 +619,21 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
             while (e < order.size() && cnt[static_cast<size_t>(order[e])] == cnt[static_cast<size_t>(order[i])]) ++e;
             std::vector<int32_t> pool(order.begin() + static_cast<std::ptrdiff_t>(i), order.begin() + static_cast<std::ptrdiff_t>(e));
             while (!pool.empty()) {
-                // rows already in the current chunk
+                // rows already in the current chunk, per residue mod 4 (-1: free); a row
+                // equal to one already there is a broadcast, not a bank conflict
                 const size_t base = out.size() / 4 * 4;
-                unsigned used_s = 0, used_b = 0;
+                int row_s[4] = {-1, -1, -1, -1}, row_b[4] = {-1, -1, -1, -1};
                 for (size_t q = base; q < out.size(); ++q) {
-                    used_s |= 1u << ((offset[d - 2] + out[q] / Bn) & 3);
-                    used_b |= 1u << ((offset[d - 1] + out[q] % Bn) & 3);
+                    const int es = offset[d - 2] + out[q] / Bn, eb = offset[d - 1] + out[q] % Bn;
+                    row_s[es & 3] = es;
+                    row_b[eb & 3] = eb;
                 }
                 size_t best = 0;
                 int best_cost = 99;
                 for (size_t q = 0; q < pool.size() && best_cost > 0; ++q) {
-                    const int cs = (used_s >> ((offset[d - 2] + pool[q] / Bn) & 3)) & 1;
-                    const int cb = (used_b >> ((offset[d - 1] + pool[q] % Bn) & 3)) & 1;
+                    const int es = offset[d - 2] + pool[q] / Bn, eb = offset[d - 1] + pool[q] % Bn;
+                    const int cs = row_s[es & 3] >= 0 && row_s[es & 3] != es;
+                    const int cb = row_b[eb & 3] >= 0 && row_b[eb & 3] != eb;
                     if (cs + cb < best_cost) {
                         best_cost = cs + cb;
                         best = q;
@@ -682,14 +685,20 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
             std::vector<int32_t> pool(gi.begin() + static_cast<std::ptrdiff_t>(i), gi.begin() + static_cast<std::ptrdiff_t>(e));
             while (!pool.empty()) {
                 const size_t pos = out.size(), blk = pos / 8 * 8;
-                std::vector<unsigned> used(static_cast<size_t>(nu), 0u);
+                std::vector<int> used(static_cast<size_t>(nu) * 4, -1);  // [level][residue] -> row
                 for (size_t q = blk + pos % 2; q < pos; q += 2)
-                    for (int l = 0; l < nu; ++l) used[l] |= 1u << ((offset[l] + at(groups[out[q]].r0, l)) & 3);
+                    for (int l = 0; l < nu; ++l) {
+                        const int e = offset[l] + at(groups[out[q]].r0, l);
+                        used[static_cast<size_t>(l) * 4 + (e & 3)] = e;
+                    }
                 size_t best = 0;
                 int best_cost = 1 << 20;
                 for (size_t q = 0; q < pool.size() && best_cost > 0; ++q) {
                     int cost = 0;
-                    for (int l = 0; l < nu; ++l) cost += (used[l] >> ((offset[l] + at(groups[pool[q]].r0, l)) & 3)) & 1;
+                    for (int l = 0; l < nu; ++l) {
+                        const int e = offset[l] + at(groups[pool[q]].r0, l), u = used[static_cast<size_t>(l) * 4 + (e & 3)];
+                        cost += u >= 0 && u != e;
+                    }
                     if (cost < best_cost) {
                         best_cost = cost;
                         best = q;
