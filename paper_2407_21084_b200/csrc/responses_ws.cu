@@ -109,7 +109,7 @@ __device__ __forceinline__ double ldg_stream(const double* p) {
 template <int D>
 struct WsSmem {
     double ypart[3][kWsConsumers][kWsPaths];  // per consumer warp, slot j % 3
-    double x[2][kWsPaths][D];                  // X_j and X_{j+1}, alternating
+    double x[2][D][kWsPaths];                  // X_j and X_{j+1}, alternating ([l][path]: lanes on consecutive banks)
     double w0[kWsPaths], dsum[kWsPaths], term[kWsPaths];
     double wq[3][kWsPaths], lq[3][kWsPaths], dpre[3][kWsPaths];  // x-only parts, slot j % 3
     int bad[kWsPaths];
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
     // start points X_i ~ nu: draws 0..D-1 of the path's stream (solver.cpp:150-152)
     for (int l = pw; l < D; l += kWsProducers) {
         const double x = measure_inv_cdf<GEN>(a.meas, u64_to_uniform(stream_u64_at(a.seed, sid, l)), l);
-        sm.x[0][p][l] = x;
+        sm.x[0][l][p] = x;
         if (a.cloud && live)
             a.cloud[l * a.n_owned + q] = a.cloud_cos ? cos(DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, x, l))) : x;
     }
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
     if (pw == 0) {
         double x[D];
 #pragma unroll
-        for (int l = 0; l < D; ++l) x[l] = sm.x[0][p][l];
+        for (int l = 0; l < D; ++l) x[l] = sm.x[0][l][p];
         sm.w0[p] = damping_weight<D>(x, a.q);
         sm.dsum[p] = 0.0;
     }
@@ -504,17 +504,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             const double nrm = 0.001 * (j + l);
 #endif
             const double dw = DMUL(a.sqrt_dt, nrm);
-            const double xo = sm.x[src][p][l];
+            const double xo = sm.x[src][l][p];
             const double v = euler_coord(a.prob, xo, dw, l, a.dt);
-            sm.x[src ^ 1][p][l] = v;
+            sm.x[src ^ 1][l][p] = v;
             if ((!isfinite(v) || fabs(v) > a.prob.state_bound) && sm.bad[p] == 0) sm.bad[p] = j + 1;
         }
 #ifdef QRMC_WS_CLOCKS
-        const long long e0 = clk_dep(sm.x[src ^ 1][p][pw]);  // Euler done (own value)
+        const long long e0 = clk_dep(sm.x[src ^ 1][pw][p]);  // Euler done (own value)
 #endif
         bar_sync(kBarProd, kProdThreads);
 #ifdef QRMC_WS_CLOCKS
-        const long long e1 = clk_dep(*reinterpret_cast<volatile double*>(&sm.x[src ^ 1][p][(pw + 1) % D]));
+        const long long e1 = clk_dep(*reinterpret_cast<volatile double*>(&sm.x[src ^ 1][(pw + 1) % D][p]));
 #endif
         if (pw == 0) {
             // the GEMM of evaluation j-2 has released table buffer j & 1
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             const int kind = pw - 1, c = j % 3;
             double xv[D];
 #pragma unroll
-            for (int l = 0; l < D; ++l) xv[l] = sm.x[kind == 2 ? src : src ^ 1][p][l];
+            for (int l = 0; l < D; ++l) xv[l] = sm.x[kind == 2 ? src : src ^ 1][l][p];
             if (kind == 0) {
                 if (j + 1 == N)
                     sm.term[p] = terminal<D>(a.prob, xv);
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_responses_ws(const StepArgs a, 
             bar_sync(kBarProd, kProdThreads);
             double* tb = tabs + (j & 1) * tab_elems;
             for (int l = pw; l < D; l += kWsProducers) {
-                const double th = DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, sm.x[src ^ 1][p][l], l));
+                const double th = DMUL(3.14159265358979323846, measure_cdf<GEN>(a.meas, sm.x[src ^ 1][l][p], l));
 #ifndef QRMC_WS_EXP_NOTAB
                 ws_table(th, m.kmax[l], m.offset[l], p, tb);
 #else
