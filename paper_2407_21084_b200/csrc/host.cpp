@@ -646,6 +646,28 @@ MmaLayout build_mma_layout(const Gamma& g, const int* offset, const MmaLayoutOpt
         }
         order.swap(out);
     }
+    if (std::getenv("QRMC_DEBUG_LAYOUT")) {
+        // 4-term chunks whose s (b) rows differ but share a residue mod 4, weighted by the
+        // number of groups that read the chunk (the pair count of its first term)
+        double w_all = 0, w_s = 0, w_b = 0;
+        for (size_t c = 0; c * 4 < order.size(); ++c) {
+            int rs[4] = {-1, -1, -1, -1}, rb[4] = {-1, -1, -1, -1};
+            bool cs = false, cb = false;
+            for (size_t q = 4 * c; q < std::min(order.size(), 4 * c + 4); ++q) {
+                const int es = offset[d - 2] + order[q] / Bn, eb = offset[d - 1] + order[q] % Bn;
+                cs |= rs[es & 3] >= 0 && rs[es & 3] != es;
+                cb |= rb[eb & 3] >= 0 && rb[eb & 3] != eb;
+                rs[es & 3] = es;
+                rb[eb & 3] = eb;
+            }
+            const double w = cnt[static_cast<size_t>(order[4 * c])];
+            w_all += w;
+            w_s += cs ? w : 0;
+            w_b += cb ? w : 0;
+        }
+        std::fprintf(stderr, "terms %zu: weighted chunks with s conflicts %.3f, b conflicts %.3f\n", order.size(),
+                     w_s / w_all, w_b / w_all);
+    }
     std::vector<int32_t> rank(static_cast<size_t>(S) * Bn, -1);
     for (size_t t = 0; t < order.size(); ++t) rank[static_cast<size_t>(order[t])] = static_cast<int32_t>(t);
     for (const Grp& gr : groups)
