@@ -516,7 +516,7 @@ ProjectItems build_project_items(const Gamma& g, const int* offset) {
 // hyperbolic index sets) every group is then a prefix of that order, which is
 // checked here -- ok = false sends the plan to the series-program K1.
 #ifndef QRMC_MMA_BANK_ORDER
-#define QRMC_MMA_BANK_ORDER 0
+#define QRMC_MMA_BANK_ORDER 1  // bank-aware term/group order for the ring kernel too (d=6: K1 -5%)
 #endif
 struct MmaLayoutOpts {
     int warps = kMmaWarps;      // GEMM warps the units are balanced over
