@@ -30,18 +30,29 @@ def main():
         a[0] += 1
         a[1] += v * scale
     tot = sum(v[1] for v in agg.values()) or 1.0
-    ev = {}
+    ev, dim = {}, None
     if len(sys.argv) > 2:
         line = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
         ks = line.get("kernel_seconds_per_solve", {})
         et = sum(ks.values()) or 1.0
         ev = {k: v / et for k, v in ks.items()}
-    print("| kernel | launches | total s (ncu) | share (ncu) | share in bench (CUDA events) |")
-    print("|---|---|---|---|---|")
+        dim = line.get("config", {}).get("d")
+    # the headline workload's kernels (template dimension = its d): their ncu share among
+    # themselves, beside the bench's CUDA-event share
+    def headline(k):
+        base = k.split("<")[0]
+        if base not in ev:
+            return False
+        return "<" not in k or dim is None or k.split("<")[1].split(",")[0].split(">")[0].strip() == str(dim)
+    hl = sum(t for k, (n, t) in agg.items() if headline(k)) or 1.0
+    print("| kernel | launches | total s (ncu) | share of all (ncu) | share of the headline solve (ncu) | share in bench (CUDA events) |")
+    print("|---|---|---|---|---|---|")
     for k, (n, t) in agg.items():
         base = k.split("<")[0]
-        e = f"{100 * ev[base]:.1f}%" if base in ev else "-"
-        print(f"| {k} | {n} | {t:.3f} | {100 * t / tot:.1f}% | {e} |")
+        h = headline(k)
+        e = f"{100 * ev[base]:.1f}%" if h else "-"
+        hs = f"{100 * t / hl:.1f}%" if h else "-"
+        print(f"| {k} | {n} | {t:.3f} | {100 * t / tot:.1f}% | {hs} | {e} |")
 
 
 if __name__ == "__main__":
