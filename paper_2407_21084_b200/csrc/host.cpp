@@ -1455,9 +1455,12 @@ std::unique_ptr<qrmc_gpu_plan> make_plan(qrmc_gpu_session* s, const qrmc_problem
                 // K2 on the tensor cores (QRMC_K2=series forces the series K2)
                 const char* k2 = std::getenv("QRMC_K2");
                 // QRMC_K2_BATCH=16 forces the narrow batch (tests: both give the same bits)
+                // and QRMC_K2_BATCH=24 the wide one when it fits. Default: 24 paths for d <= 4 (Gamma_H(4,100):
+                // K2 -4..6%), 16 beyond (Gamma_H(6,64): 0.338 vs 0.347 s, d = 5, 6 otherwise equal)
                 const char* k2b = std::getenv("QRMC_K2_BATCH");
                 int pbatch = project_mma_batch(off, static_cast<size_t>(optin));
-                if (pbatch && k2b && std::atoi(k2b) == kProjBatchNarrow) pbatch = kProjBatchNarrow;
+                const int want = k2b ? std::atoi(k2b) : (d <= 4 ? kProjBatchWide : kProjBatchNarrow);
+                if (pbatch && want == kProjBatchNarrow) pbatch = kProjBatchNarrow;
                 const size_t psmem = pbatch ? project_mma_smem_bytes(off, pbatch) : 0;
                 if (!(k2 && std::strcmp(k2, "series") == 0) && pbatch && L.proj_parts > 0) {
                     P->use_proj_mma = true;

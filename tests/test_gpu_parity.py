@@ -307,11 +307,12 @@ def test_k2_lane_split_matches_port(L, port, monkeypatch, split):
 
 @pytest.mark.parametrize("dim,deg,paths", [(3, 8, 5000), (4, 100, 3000), (6, 16, 2051)])
 def test_k2_batch_width_does_not_change_bits(L, monkeypatch, dim, deg, paths):
-    # K2 stages 24 paths per shared-memory batch (16 when those tables do not fit);
+    # K2 stages 24 or 16 paths per shared-memory batch (host.cpp picks by d and fit);
     # a chunk's short last batch adds exact zeros, so the tensor-core sum over paths
     # runs in the same order either way and the coefficients agree bit for bit
     prob = _abi.sin_bench_problem(dim)
     cfg = _abi.ConfigHolder(steps=3, paths=paths, damping=5.1, seed=5, gamma_kind=2, degrees=[deg])
+    monkeypatch.setenv("QRMC_K2_BATCH", "24")
     wide, sw, _ = api.backward_solve(prob, cfg)
     monkeypatch.setenv("QRMC_K2_BATCH", "16")
     assert _kernel_names(prob, cfg)[1] == "k_project_mma"
