@@ -522,7 +522,10 @@ void launch_step_t(const SrmcDev& s, const double* next, double* y, double* z, b
     // 4 lanes per hypercube, 8 hypercubes per warp -- only when the range still fills the
     // GPU with an eighth as many warps (64^2 cells at M=100: 1.33e10 -> 1.1e10 with a warp
     // per cell; config 4: 4 lanes 1.92e10, 8 lanes 1.83e10, 2 / 1 lanes +0.5 / +1%)
-    if (s.M < 256 && s.cells >= 32768) {  // by the TOTAL cell count: a shard computes exactly what the whole solve does
+    // (also for M < 2048 without a Z pass: config 2, M = 1000, 2.25e10 -> 2.35e10 -- 250
+    // iterations per lane, none half-empty; the Bergman Z pass keeps a warp per cell for its
+    // path cache unless M < 256)
+    if (s.cells >= 32768 && s.M < (zpass ? 256 : 2048)) {  // by the TOTAL cell count: a shard computes exactly what the whole solve does
 #ifndef QRMC_SRMC_SUBG
 #define QRMC_SRMC_SUBG 4
 #endif

@@ -134,6 +134,8 @@ PARITY_CASES = [
     ("sin-d3-lp1", lambda: srmc.sin_bench_problem(3), dict(steps=3, cells_per_dim=5, paths_per_cell=37, basis=srmc.LP1)),
     # >= 32768 cells and M < 256: 4 lanes per hypercube (8 per warp), 33^3 leaves a tail group
     ("sin-d3-lp1-subwarp", lambda: srmc.sin_bench_problem(3), dict(steps=2, cells_per_dim=33, paths_per_cell=40, basis=srmc.LP1, want_z=True)),
+    # M >= 256 without a Z pass also runs 4 lanes per hypercube (M < 2048)
+    ("sin-d3-lp1-z-subwarp-m260", lambda: srmc.sin_bench_problem(3), dict(steps=2, cells_per_dim=33, paths_per_cell=260, basis=srmc.LP1, want_z=True)),
     ("bergman-d3-lp1-subwarp", lambda: _bergman(3, 0.01, 0.06), dict(steps=2, cells_per_dim=33, paths_per_cell=24, basis=srmc.LP1, lo=_box()[0], hi=_box()[1])),
     ("sin-d6-lp1-one-cell", lambda: srmc.sin_bench_problem(6), dict(steps=3, cells_per_dim=1, paths_per_cell=300, basis=srmc.LP1)),
     ("sin-d3-lp1-z-morton", lambda: srmc.sin_bench_problem(3), dict(steps=3, cells_per_dim=4, paths_per_cell=40, basis=srmc.LP1, want_z=True)),
